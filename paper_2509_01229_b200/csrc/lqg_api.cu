@@ -1,0 +1,681 @@
+// C-ABI implementation of include/lqg.h: validation with the reference's
+// semantics, host prepack into the device image, launch configuration and
+// the host-buffer staging path. See lqg_gemm.cuh for the kernel design.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/lqg.h"
+#include "lqg_aux.cuh"
+#include "lqg_gemm.cuh"
+#include "lqg_layout.h"
+
+using namespace lqg;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+
+struct Status {
+    int code;
+};
+
+int set_err(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define LQG_CUDA(expr)                                                                       \
+    do {                                                                                     \
+        cudaError_t e__ = (expr);                                                            \
+        if (e__ != cudaSuccess)                                                              \
+            return set_err(LQG_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e__)); \
+    } while (0)
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+int check_device(int dev, int* num_sms) {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+        return set_err(LQG_EUNSUPPORTED, "no CUDA device available (liblqg has no CPU fallback)");
+    if (dev < 0 || dev >= count) return set_err(LQG_EVALIDATION, "device index out of range");
+    int major = 0, minor = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    if (major != 10 || minor != 0)
+        return set_err(LQG_EUNSUPPORTED, "liblqg is built for sm_100a (B200); device has sm_" +
+                                             std::to_string(major) + std::to_string(minor));
+    if (num_sms) cudaDeviceGetAttribute(num_sms, cudaDevAttrMultiProcessorCount, dev);
+    return LQG_OK;
+}
+
+// ---------------------------------------------------------------- tensor maps
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    return fn;
+}
+
+// ---------------------------------------------------------------- workspace
+constexpr uint32_t kMaxSlots = 160;  // >= SM count of any sm_100 part
+constexpr uint64_t kSlotInts = 256ull * kTileN;
+
+}  // namespace
+
+struct lqg_workspace {
+    int device = 0;
+    int32_t* ws = nullptr;
+    uint32_t* counters = nullptr;
+};
+
+struct lqg_weights {
+    int device = 0;
+    int num_sms = 148;
+    ImageGeom geom{};
+    uint8_t* d_img = nullptr;
+    uint64_t img_bytes = 0;
+    float* d_cs = nullptr;
+    lqg_workspace* ws = nullptr;
+    // host-call staging
+    int8_t* d_x = nullptr;
+    size_t x_cap = 0;
+    float* d_ts = nullptr;
+    size_t ts_cap = 0;
+    void* d_y = nullptr;
+    size_t y_cap = 0;
+};
+
+namespace {
+
+int workspace_create(int dev, lqg_workspace** out) {
+    auto* w = new lqg_workspace();
+    w->device = dev;
+    DeviceGuard g(dev);
+    if (cudaMalloc(&w->ws, kMaxSlots * kSlotInts * 4) != cudaSuccess ||
+        cudaMalloc(&w->counters, kMaxSlots * 4) != cudaSuccess) {
+        cudaFree(w->ws);
+        delete w;
+        return set_err(LQG_ECUDA, "workspace allocation failed");
+    }
+    cudaMemset(w->ws, 0, kMaxSlots * kSlotInts * 4);
+    cudaMemset(w->counters, 0, kMaxSlots * 4);
+    if (cudaDeviceSynchronize() != cudaSuccess) return set_err(LQG_ECUDA, "workspace memset failed");
+    *out = w;
+    return LQG_OK;
+}
+
+// Reference validation, bundle.cpp:89-135 (+ FragmentDescriptor::validate,
+// layout.cpp:10-22).
+int validate_bundle(const lqg_bundle_view& b) {
+    if (b.n < 1 || b.k < 1) return set_err(LQG_EVALIDATION, "bundle dimensions must be >= 1");
+    if (b.group_size < 1) return set_err(LQG_EVALIDATION, "group_size must be >= 1");
+    if (b.k % b.group_size != 0)
+        return set_err(LQG_EVALIDATION, "k = " + std::to_string(b.k) +
+                                            " not divisible by group_size = " +
+                                            std::to_string(b.group_size));
+    if (b.layout > 1) return set_err(LQG_EVALIDATION, "unknown layout flag " + std::to_string(b.layout));
+    if (b.layout == LQG_LAYOUT_DUAL_MMA) {
+        const auto& d = b.fragment;
+        const uint32_t slab = uint32_t(d.mma_m) * d.mma_k;
+        const uint32_t per_group =
+            uint32_t(d.warps_per_group) * d.threads_per_warp * d.elements_per_thread_per_mma;
+        if (slab != per_group)
+            return set_err(LQG_EVALIDATION, "fragment descriptor mismatch: mma_m*mma_k = " +
+                                                std::to_string(slab) + " but group covers " +
+                                                std::to_string(per_group) + " elements");
+        if (d.dual_k_span != 2 * d.mma_k)
+            return set_err(LQG_EVALIDATION, "dual_k_span must be 2*mma_k");
+        if (!d.warps_per_group || !d.threads_per_warp || !d.mma_m || !d.mma_k)
+            return set_err(LQG_EVALIDATION, "fragment descriptor has a zero field");
+        if (b.n % d.mma_m != 0)
+            return set_err(LQG_EVALIDATION,
+                           "dual-MMA layout needs n divisible by " + std::to_string(d.mma_m));
+        if (b.k % d.dual_k_span != 0)
+            return set_err(LQG_EVALIDATION,
+                           "dual-MMA layout needs k divisible by " + std::to_string(d.dual_k_span));
+        if (b.group_size % d.dual_k_span != 0)
+            return set_err(LQG_EVALIDATION, "dual-MMA layout needs group_size divisible by " +
+                                                std::to_string(d.dual_k_span) +
+                                                " so each record word pair stays within one group");
+    }
+    const uint64_t nk = uint64_t(b.n) * b.k;
+    if (!b.packed_weights || b.packed_bytes != (nk + 1) / 2)
+        return set_err(LQG_EVALIDATION, "packed weight payload has wrong size");
+    const uint32_t gpr = b.k / b.group_size;
+    const uint64_t ng = uint64_t(b.n) * gpr;
+    if (!b.group_scales || !b.group_offsets || b.n_groups != ng)
+        return set_err(LQG_EVALIDATION, "group parameter arrays have wrong size");
+    if (!b.channel_scales) return set_err(LQG_EVALIDATION, "channel scale array has wrong size");
+    for (uint64_t i = 0; i < ng; ++i) {
+        const uint32_t row = uint32_t(i / gpr), g = uint32_t(i % gpr);
+        if (b.group_scales[i] < 1 || b.group_scales[i] > 16)
+            return set_err(LQG_EVALIDATION, "group scale " + std::to_string(int(b.group_scales[i])) +
+                                                " out of [1,16] at row " + std::to_string(row) +
+                                                " group " + std::to_string(g));
+        if (b.group_offsets[i] < 9 || b.group_offsets[i] > 247)
+            return set_err(LQG_EVALIDATION, "group offset " +
+                                                std::to_string(int(b.group_offsets[i])) +
+                                                " out of [9,247] at row " + std::to_string(row) +
+                                                " group " + std::to_string(g));
+    }
+    for (uint32_t r = 0; r < b.n; ++r) {
+        const float s = b.channel_scales[r];
+        if (!(s > 0.0f) || !std::isfinite(s))
+            return set_err(LQG_EVALIDATION, "channel scale at row " + std::to_string(r) +
+                                                " must be positive and finite");
+    }
+    return LQG_OK;
+}
+
+int device_layout_supported(uint32_t g) {
+    if (g % 32 != 0)
+        return set_err(LQG_EVALIDATION, "the sm_100a device layout needs group_size % 32 == 0 (got " +
+                                            std::to_string(g) + ")");
+    return LQG_OK;
+}
+
+// Logical code (row, col) of a bundle in either layout (bundle.cpp:59-87).
+struct CodeReader {
+    const lqg_bundle_view& b;
+    uint8_t at(uint32_t row, uint32_t col) const {
+        if (b.layout == LQG_LAYOUT_PLAIN) {
+            const uint64_t idx = uint64_t(row) * b.k + col;
+            const uint8_t byte = b.packed_weights[idx / 2];
+            return (idx % 2 == 0) ? (byte & 0x0F) : (byte >> 4);
+        }
+        const auto& d = b.fragment;
+        const uint32_t band = row / d.mma_m, r_in = row % d.mma_m;
+        const uint32_t warp = r_in / 16, r = (r_in % 16) / 8, row_quarter = r_in % 8;
+        const uint32_t pair = col / d.dual_k_span, col_in = col % d.dual_k_span;
+        const uint32_t half = col_in / d.mma_k, c32 = col_in % d.mma_k;
+        const uint32_t bsel = c32 / 16;
+        const uint32_t thread = 4 * row_quarter + (c32 % 16) / 4;
+        const uint32_t j = c32 % 4;
+        const uint64_t band_bytes = uint64_t(d.mma_m) * b.k / 2;
+        const uint64_t record = (uint64_t(pair) * d.warps_per_group + warp) * d.threads_per_warp + thread;
+        const uint64_t byte_idx = band * band_bytes + record * 16 + (2 * half + r) * 4 + j;
+        const uint8_t byte = b.packed_weights[byte_idx];
+        return bsel == 0 ? (byte & 0x0F) : (byte >> 4);
+    }
+};
+
+// Host prepack: bundle (either layout) -> device image (lqg_layout.h).
+void prepack_host(const lqg_bundle_view& b, const ImageGeom& G, std::vector<uint8_t>& img) {
+    img.assign(uint64_t(G.NT) * G.KB * G.chunk_bytes, 0);
+    // padding params (s=1, a=128)
+    for (uint64_t ch = 0; ch < uint64_t(G.NT) * G.KB; ++ch)
+        for (uint32_t i = 0; i < 128 * G.P; ++i) {
+            uint8_t* p = img.data() + ch * G.chunk_bytes + kCodeBytes + 2 * i;
+            p[0] = 1;
+            p[1] = 128;
+        }
+    CodeReader rd{b};
+    const uint32_t gpr = b.k / b.group_size;
+    std::vector<uint8_t> rowcodes(b.k);
+    for (uint32_t row = 0; row < b.n; ++row) {
+        if (b.layout == LQG_LAYOUT_PLAIN && (uint64_t(row) * b.k) % 2 == 0) {
+            const uint8_t* src = b.packed_weights + uint64_t(row) * b.k / 2;
+            for (uint32_t c = 0; c + 1 < b.k; c += 2) {
+                rowcodes[c] = src[c / 2] & 0x0F;
+                rowcodes[c + 1] = src[c / 2] >> 4;
+            }
+            if (b.k % 2) rowcodes[b.k - 1] = src[(b.k - 1) / 2] & 0x0F;
+        } else {
+            for (uint32_t c = 0; c < b.k; ++c) rowcodes[c] = rd.at(row, c);
+        }
+        for (uint32_t k0 = 0; k0 < b.k; k0 += 8) {
+            uint32_t word = 0;
+            for (uint32_t j = 0; j < 4; ++j) {
+                const uint32_t lo = k0 + j < b.k ? rowcodes[k0 + j] : 0;
+                const uint32_t hi = k0 + j + 4 < b.k ? rowcodes[k0 + j + 4] : 0;
+                word |= (lo | (hi << 4)) << (8 * j);
+            }
+            const uint32_t kb = k0 / kKBlock, c = (k0 % kKBlock) / 32, wsub = (k0 % 32) / 8;
+            std::memcpy(img.data() + code_offset(G.chunk_bytes, G.KB, row, kb, c) + wsub * 4, &word, 4);
+        }
+        const uint32_t sub_per_p = kSubBlocks / G.P;
+        for (uint32_t k0 = 0; k0 < b.k; k0 += 32) {
+            const uint32_t kb = k0 / kKBlock, c = (k0 % kKBlock) / 32;
+            if (c % sub_per_p) continue;
+            const uint32_t gi = k0 / b.group_size;
+            uint8_t* p = img.data() + param_offset(G.chunk_bytes, G.KB, row, kb, c / sub_per_p);
+            p[0] = b.group_scales[uint64_t(row) * gpr + gi];
+            p[1] = b.group_offsets[uint64_t(row) * gpr + gi];
+        }
+    }
+}
+
+int alloc_weights(int dev, const ImageGeom& G, lqg_weights** out) {
+    auto* w = new lqg_weights();
+    w->device = dev;
+    w->geom = G;
+    w->img_bytes = uint64_t(G.NT) * G.KB * G.chunk_bytes;
+    int rc = check_device(dev, &w->num_sms);
+    if (rc) {
+        delete w;
+        return rc;
+    }
+    DeviceGuard g(dev);
+    if (cudaMalloc(&w->d_img, w->img_bytes) != cudaSuccess ||
+        cudaMalloc(&w->d_cs, uint64_t(G.NT) * kTileN * 4) != cudaSuccess) {
+        cudaFree(w->d_img);
+        delete w;
+        return set_err(LQG_ECUDA, "weight image allocation failed");
+    }
+    rc = workspace_create(dev, &w->ws);
+    if (rc) {
+        cudaFree(w->d_img);
+        cudaFree(w->d_cs);
+        delete w;
+        return rc;
+    }
+    *out = w;
+    return LQG_OK;
+}
+
+uint32_t choose_bn(uint32_t m, uint32_t* mt) {
+    const uint32_t MT = (m + 255) / 256;
+    const uint32_t per = (m + MT - 1) / MT;
+    *mt = MT;
+    return std::max(16u, (per + 15) / 16 * 16);
+}
+
+std::once_flag g_attr_once[64];
+
+int launch_gemm(const lqg_weights* w, const int8_t* d_x, int64_t ldx, const float* d_ts, uint32_t m,
+                void* d_out, int64_t ldo, uint32_t out_kind, lqg_workspace* ws, cudaStream_t stream) {
+    const ImageGeom& G = w->geom;
+    if (m < 1) return set_err(LQG_EVALIDATION, "activation dimensions must be >= 1");
+    if (int64_t(G.k) * 127 * 127 >= (int64_t(1) << 31))
+        return set_err(LQG_EVALIDATION, "k = " + std::to_string(G.k) +
+                                            " risks 32-bit accumulator overflow (k*127*127 >= 2^31)");
+    if (!d_x || !d_out || (out_kind != kOutAcc && !d_ts))
+        return set_err(LQG_EVALIDATION, "null device pointer");
+    if (ldx < int64_t(G.k) || ldx % 16 != 0 || (reinterpret_cast<uintptr_t>(d_x) % 16) != 0)
+        return set_err(LQG_EVALIDATION, "activation pitch must be >= k and 16-byte aligned");
+    if (ldo < int64_t(G.n)) return set_err(LQG_EVALIDATION, "output pitch must be >= n");
+    if (ws && ws->device != w->device)
+        return set_err(LQG_EVALIDATION, "workspace lives on another device");
+    lqg_workspace* W = ws ? ws : w->ws;
+
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) return set_err(LQG_ECUDA, "cuTensorMapEncodeTiled unavailable");
+
+    uint32_t MT;
+    const uint32_t BN = choose_bn(m, &MT);
+    CUtensorMap tmap;
+    const cuuint64_t dims[2] = {G.k, m};
+    const cuuint64_t strides[1] = {cuuint64_t(ldx)};
+    const cuuint32_t box[2] = {kKBlock, BN};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult cr = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(d_x), dims,
+                      strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS)
+        return set_err(LQG_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(int(cr)) + ")");
+
+    GemmParams p{};
+    p.wimg = w->d_img;
+    p.cs = w->d_cs;
+    p.ts = d_ts;
+    p.out = d_out;
+    p.ldo = ldo;
+    p.ws = W->ws;
+    p.counters = W->counters;
+    p.M = m;
+    p.N = G.n;
+    p.KB = G.KB;
+    p.NT = G.NT;
+    p.MT = MT;
+    p.BN = BN;
+    p.P = G.P;
+    p.chunk_bytes = G.chunk_bytes;
+    p.out_kind = out_kind;
+    p.stage_bytes = (BN * kKBlock + G.chunk_bytes + 1023) / 1024 * 1024;
+    const uint32_t budget = 227 * 1024 - 2048;
+    p.stages = std::min<uint32_t>(kMaxStages, budget / p.stage_bytes);
+    if (p.stages < 2) return set_err(LQG_EVALIDATION, "tile configuration does not fit shared memory");
+    p.total_iters = uint64_t(MT) * G.NT * G.KB;
+    const uint32_t grid = static_cast<uint32_t>(
+        std::min<uint64_t>(std::min<uint32_t>(w->num_sms, kMaxSlots), p.total_iters));
+    const size_t smem = size_t(p.stages) * p.stage_bytes + 1024 + 1024;
+
+    DeviceGuard dg(w->device);
+    cudaError_t e = cudaSuccess;
+    std::call_once(g_attr_once[w->device % 64], [&] {
+        e = cudaFuncSetAttribute(lqg_w4a8_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 227 * 1024);
+    });
+    if (e != cudaSuccess) return set_err(LQG_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+    lqg_w4a8_gemm_kernel<<<grid, kThreads, smem, stream>>>(tmap, p);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    LQG_CUDA(cudaGetLastError());
+    return LQG_OK;
+}
+
+int ensure_cap(void** ptr, size_t* cap, size_t need) {
+    if (*cap >= need) return LQG_OK;
+    cudaFree(*ptr);
+    *ptr = nullptr;
+    *cap = 0;
+    if (cudaMalloc(ptr, need) != cudaSuccess) return set_err(LQG_ECUDA, "staging allocation failed");
+    *cap = need;
+    return LQG_OK;
+}
+
+size_t out_elem_bytes(int y_dtype) { return y_dtype == LQG_Y_F32 ? 4 : 2; }
+
+int out_kind_of(int y_dtype, uint32_t* kind) {
+    switch (y_dtype) {
+        case LQG_Y_F32: *kind = kOutF32; return LQG_OK;
+        case LQG_Y_F16: *kind = kOutF16; return LQG_OK;
+        case LQG_Y_BF16: *kind = kOutBF16; return LQG_OK;
+    }
+    return set_err(LQG_EVALIDATION, "unknown output dtype " + std::to_string(y_dtype));
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* lqg_last_error(void) { return g_err.c_str(); }
+const char* lqg_version(void) { return "lqg 0.1 (sm_100a, tcgen05 kind::i8, TMEM-A LiquidQuant mainloop)"; }
+uint64_t lqg_kernel_launch_count(void) { return g_launches.load(); }
+
+int lqg_bundle_validate(const lqg_bundle_view* bundle) {
+    if (!bundle) return set_err(LQG_EVALIDATION, "null argument");
+    return validate_bundle(*bundle);
+}
+
+int lqg_weights_create(const lqg_bundle_view* bundle, int device, lqg_weights** out) {
+    if (!bundle || !out) return set_err(LQG_EVALIDATION, "null argument");
+    int rc = validate_bundle(*bundle);
+    if (rc) return rc;
+    rc = device_layout_supported(bundle->group_size);
+    if (rc) return rc;
+    const ImageGeom G = make_geom(bundle->n, bundle->k, bundle->group_size);
+    lqg_weights* w = nullptr;
+    rc = alloc_weights(device, G, &w);
+    if (rc) return rc;
+    std::vector<uint8_t> img;
+    prepack_host(*bundle, G, img);
+    std::vector<float> cs(uint64_t(G.NT) * kTileN, 1.0f);
+    std::memcpy(cs.data(), bundle->channel_scales, bundle->n * 4);
+    DeviceGuard g(device);
+    if (cudaMemcpy(w->d_img, img.data(), img.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(w->d_cs, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
+        lqg_weights_destroy(w);
+        return set_err(LQG_ECUDA, "weight upload failed");
+    }
+    *out = w;
+    return LQG_OK;
+}
+
+int lqg_weights_quantize(const float* d_w, int64_t ldw, uint32_t n, uint32_t k, uint32_t group_size,
+                         void* stream, lqg_weights** out) {
+    if (!d_w || !out) return set_err(LQG_EVALIDATION, "null argument");
+    if (n < 1 || k < 1) return set_err(LQG_EVALIDATION, "weight matrix dimensions must be >= 1");
+    if (group_size < 1) return set_err(LQG_EVALIDATION, "group_size must be >= 1");
+    if (k % group_size != 0)
+        return set_err(LQG_EVALIDATION, "k = " + std::to_string(k) + " not divisible by group_size = " +
+                                            std::to_string(group_size));
+    if (ldw < int64_t(k)) return set_err(LQG_EVALIDATION, "weight pitch must be >= k");
+    int rc = device_layout_supported(group_size);
+    if (rc) return rc;
+    cudaPointerAttributes attr;
+    if (cudaPointerGetAttributes(&attr, d_w) != cudaSuccess || attr.type != cudaMemoryTypeDevice)
+        return set_err(LQG_EVALIDATION, "weights must be a device pointer");
+    const ImageGeom G = make_geom(n, k, group_size);
+    lqg_weights* w = nullptr;
+    rc = alloc_weights(attr.device, G, &w);
+    if (rc) return rc;
+    DeviceGuard g(attr.device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int8_t* q = nullptr;
+    unsigned long long* bad = nullptr;
+    auto cleanup = [&] {
+        cudaFree(q);
+        cudaFree(bad);
+    };
+    if (cudaMalloc(&q, uint64_t(n) * k) != cudaSuccess || cudaMalloc(&bad, 8) != cudaSuccess) {
+        cleanup();
+        lqg_weights_destroy(w);
+        return set_err(LQG_ECUDA, "quantizer scratch allocation failed");
+    }
+    cudaMemsetAsync(bad, 0xFF, 8, st);
+    {
+        const uint64_t nch = uint64_t(G.NT) * G.KB;
+        fill_image_kernel<<<1184, 256, 0, st>>>(w->d_img, nch, G.chunk_bytes);
+        std::vector<float> ones(uint64_t(G.NT) * kTileN, 1.0f);
+        cudaMemcpyAsync(w->d_cs, ones.data(), ones.size() * 4, cudaMemcpyHostToDevice, st);
+        quantize_level1_kernel<<<n, 256, 0, st>>>(d_w, ldw, n, k, q, w->d_cs, bad);
+        const uint64_t warps = uint64_t(n) * (k / group_size);
+        quantize_level2_pack_kernel<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, st>>>(
+            q, n, k, group_size, w->d_img, G.chunk_bytes, G.KB, G.P);
+        g_launches.fetch_add(3, std::memory_order_relaxed);
+    }
+    unsigned long long h_bad = 0;
+    cudaError_t e = cudaMemcpyAsync(&h_bad, bad, 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cleanup();
+    if (e != cudaSuccess) {
+        lqg_weights_destroy(w);
+        return set_err(LQG_ECUDA, std::string("weight quantization failed: ") + cudaGetErrorString(e));
+    }
+    if (h_bad != ~0ull) {
+        lqg_weights_destroy(w);
+        return set_err(LQG_EVALIDATION, "non-finite weight at (" + std::to_string(h_bad / k) + ", " +
+                                            std::to_string(h_bad % k) + ")");
+    }
+    *out = w;
+    return LQG_OK;
+}
+
+int lqg_weights_destroy(lqg_weights* w) {
+    if (!w) return LQG_OK;
+    DeviceGuard g(w->device);
+    cudaFree(w->d_img);
+    cudaFree(w->d_cs);
+    cudaFree(w->d_x);
+    cudaFree(w->d_ts);
+    cudaFree(w->d_y);
+    lqg_workspace_destroy(w->ws);
+    delete w;
+    return LQG_OK;
+}
+
+int lqg_weights_shape(const lqg_weights* w, uint32_t* n, uint32_t* k, uint32_t* g) {
+    if (!w) return set_err(LQG_EVALIDATION, "null handle");
+    if (n) *n = w->geom.n;
+    if (k) *k = w->geom.k;
+    if (g) *g = w->geom.g;
+    return LQG_OK;
+}
+
+uint64_t lqg_weights_device_bytes(const lqg_weights* w) {
+    return w ? w->img_bytes + uint64_t(w->geom.NT) * kTileN * 4 : 0;
+}
+
+int lqg_weights_export(const lqg_weights* w, uint8_t* packed, uint8_t* scales, uint8_t* offsets,
+                       float* cs) {
+    if (!w) return set_err(LQG_EVALIDATION, "null handle");
+    const ImageGeom& G = w->geom;
+    std::vector<uint8_t> img(w->img_bytes);
+    DeviceGuard g(w->device);
+    LQG_CUDA(cudaMemcpy(img.data(), w->d_img, img.size(), cudaMemcpyDeviceToHost));
+    if (cs) LQG_CUDA(cudaMemcpy(cs, w->d_cs, uint64_t(G.n) * 4, cudaMemcpyDeviceToHost));
+    const uint32_t gpr = G.k / G.g;
+    for (uint32_t row = 0; row < G.n; ++row) {
+        if (packed) {
+            for (uint32_t k0 = 0; k0 < G.k; k0 += 8) {
+                const uint32_t kb = k0 / kKBlock, c = (k0 % kKBlock) / 32, wsub = (k0 % 32) / 8;
+                uint32_t word;
+                std::memcpy(&word, img.data() + code_offset(G.chunk_bytes, G.KB, row, kb, c) + wsub * 4, 4);
+                for (uint32_t e = 0; e < 8 && k0 + e < G.k; ++e) {
+                    const uint32_t code = (word >> (8 * (e % 4) + 4 * (e / 4))) & 0xF;
+                    const uint64_t idx = uint64_t(row) * G.k + k0 + e;
+                    if (idx % 2 == 0)
+                        packed[idx / 2] = uint8_t((packed[idx / 2] & 0xF0) | code);
+                    else
+                        packed[idx / 2] = uint8_t((packed[idx / 2] & 0x0F) | (code << 4));
+                }
+            }
+        }
+        for (uint32_t gi = 0; gi < gpr; ++gi) {
+            const uint32_t k0 = gi * G.g;
+            const uint32_t kb = k0 / kKBlock, c = (k0 % kKBlock) / 32;
+            const uint8_t* p = img.data() + param_offset(G.chunk_bytes, G.KB, row, kb, c / (kSubBlocks / G.P));
+            if (scales) scales[uint64_t(row) * gpr + gi] = p[0];
+            if (offsets) offsets[uint64_t(row) * gpr + gi] = p[1];
+        }
+    }
+    return LQG_OK;
+}
+
+int lqg_workspace_create(int device, lqg_workspace** out) {
+    if (!out) return set_err(LQG_EVALIDATION, "null argument");
+    int rc = check_device(device, nullptr);
+    if (rc) return rc;
+    return workspace_create(device, out);
+}
+
+int lqg_workspace_destroy(lqg_workspace* ws) {
+    if (!ws) return LQG_OK;
+    DeviceGuard g(ws->device);
+    cudaFree(ws->ws);
+    cudaFree(ws->counters);
+    delete ws;
+    return LQG_OK;
+}
+
+int lqg_gemm_w4a8(const lqg_weights* w, const int8_t* d_x, int64_t ldx, const float* d_ts, uint32_t m,
+                  void* d_y, int64_t ldy, int y_dtype, lqg_workspace* ws, void* stream) {
+    if (!w) return set_err(LQG_EVALIDATION, "null handle");
+    uint32_t kind;
+    int rc = out_kind_of(y_dtype, &kind);
+    if (rc) return rc;
+    return launch_gemm(w, d_x, ldx, d_ts, m, d_y, ldy, kind, ws, static_cast<cudaStream_t>(stream));
+}
+
+int lqg_gemm_w4a8_accum(const lqg_weights* w, const int8_t* d_x, int64_t ldx, uint32_t m, int32_t* d_acc,
+                        int64_t ldacc, lqg_workspace* ws, void* stream) {
+    if (!w) return set_err(LQG_EVALIDATION, "null handle");
+    return launch_gemm(w, d_x, ldx, nullptr, m, d_acc, ldacc, kOutAcc, ws,
+                       static_cast<cudaStream_t>(stream));
+}
+
+static int host_call(const lqg_weights* wc, const int8_t* x, const float* ts, uint32_t m, void* y,
+                     uint32_t kind, size_t ebytes, cudaStream_t st) {
+    auto* w = const_cast<lqg_weights*>(wc);
+    if (!w) return set_err(LQG_EVALIDATION, "null handle");
+    if (m < 1) return set_err(LQG_EVALIDATION, "activation dimensions must be >= 1");
+    if (!x || !y || (kind != kOutAcc && !ts)) return set_err(LQG_EVALIDATION, "null host pointer");
+    const ImageGeom& G = w->geom;
+    DeviceGuard g(w->device);
+    const int64_t ldx = (int64_t(G.k) + 15) / 16 * 16;
+    int rc = ensure_cap(reinterpret_cast<void**>(&w->d_x), &w->x_cap, size_t(m) * ldx);
+    if (!rc) rc = ensure_cap(reinterpret_cast<void**>(&w->d_ts), &w->ts_cap, size_t(m) * 4);
+    if (!rc) rc = ensure_cap(&w->d_y, &w->y_cap, size_t(m) * G.n * ebytes);
+    if (rc) return rc;
+    if (ldx == int64_t(G.k)) {
+        LQG_CUDA(cudaMemcpyAsync(w->d_x, x, size_t(m) * G.k, cudaMemcpyHostToDevice, st));
+    } else {
+        LQG_CUDA(cudaMemcpy2DAsync(w->d_x, ldx, x, G.k, G.k, m, cudaMemcpyHostToDevice, st));
+    }
+    if (kind != kOutAcc)
+        LQG_CUDA(cudaMemcpyAsync(w->d_ts, ts, size_t(m) * 4, cudaMemcpyHostToDevice, st));
+    rc = launch_gemm(w, w->d_x, ldx, w->d_ts, m, w->d_y, G.n, kind, nullptr, st);
+    if (rc) return rc;
+    LQG_CUDA(cudaMemcpyAsync(y, w->d_y, size_t(m) * G.n * ebytes, cudaMemcpyDeviceToHost, st));
+    LQG_CUDA(cudaStreamSynchronize(st));
+    return LQG_OK;
+}
+
+int lqg_gemm_w4a8_host(const lqg_weights* w, const int8_t* x, const float* ts, uint32_t m, void* y,
+                       int y_dtype, void* stream) {
+    uint32_t kind;
+    int rc = out_kind_of(y_dtype, &kind);
+    if (rc) return rc;
+    return host_call(w, x, ts, m, y, kind, out_elem_bytes(y_dtype), static_cast<cudaStream_t>(stream));
+}
+
+int lqg_gemm_w4a8_accum_host(const lqg_weights* w, const int8_t* x, uint32_t m, int32_t* acc,
+                             void* stream) {
+    return host_call(w, x, nullptr, m, acc, kOutAcc, 4, static_cast<cudaStream_t>(stream));
+}
+
+int lqg_dequant_weights(const lqg_weights* w, int8_t* d_w, int64_t ldw, void* stream) {
+    if (!w || !d_w) return set_err(LQG_EVALIDATION, "null argument");
+    const ImageGeom& G = w->geom;
+    if (ldw < int64_t(G.k)) return set_err(LQG_EVALIDATION, "output pitch must be >= k");
+    DeviceGuard g(w->device);
+    const uint64_t threads = uint64_t(G.n) * G.KB * kSubBlocks;
+    dequant_image_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0,
+                           static_cast<cudaStream_t>(stream)>>>(w->d_img, G.n, G.k, G.chunk_bytes,
+                                                                G.KB, G.P, d_w, ldw);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    LQG_CUDA(cudaGetLastError());
+    return LQG_OK;
+}
+
+int lqg_quantize_activations(const float* d_x, int64_t ldx, uint32_t m, uint32_t k, int8_t* d_q,
+                             int64_t ldq, float* d_ts, int check_finite, void* stream) {
+    if (m < 1 || k < 1) return set_err(LQG_EVALIDATION, "activation dimensions must be >= 1");
+    if (!d_x || !d_q || !d_ts) return set_err(LQG_EVALIDATION, "null device pointer");
+    if (ldx < int64_t(k) || ldq < int64_t(k)) return set_err(LQG_EVALIDATION, "pitch must be >= k");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    unsigned long long* bad = nullptr;
+    if (check_finite) {
+        LQG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&bad), 8, st));
+        LQG_CUDA(cudaMemsetAsync(bad, 0xFF, 8, st));
+    }
+    quantize_activations_kernel<<<m, 256, 0, st>>>(d_x, ldx, m, k, d_q, ldq, d_ts, bad);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    LQG_CUDA(cudaGetLastError());
+    if (check_finite) {
+        unsigned long long h = 0;
+        LQG_CUDA(cudaMemcpyAsync(&h, bad, 8, cudaMemcpyDeviceToHost, st));
+        LQG_CUDA(cudaFreeAsync(bad, st));
+        LQG_CUDA(cudaStreamSynchronize(st));
+        if (h != ~0ull)
+            return set_err(LQG_EVALIDATION, "non-finite activation at (" + std::to_string(h / k) + ", " +
+                                                std::to_string(h % k) + ")");
+    }
+    return LQG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,184 @@
+// Auxiliary sm_100a kernels around the W4A8 GEMM:
+//   * image fill (padding = code 0, s=1, a=128),
+//   * the two-level LiquidQuant weight quantizer, straight into the device
+//     image (build_bundle, quant.cpp:203-232 — bit-exact),
+//   * weight dequantization to INT8 with the mainloop's own LQQ routine
+//     (reconstruct_int8, quant.cpp:234-251),
+//   * per-token activation quantization (gemm.cpp:19-47 — bit-exact).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "lqg_gemm.cuh"
+#include "lqg_layout.h"
+
+namespace lqg {
+
+// quant.hpp:33-35
+__device__ __forceinline__ int round_half_away(double v) {
+    return static_cast<int>(v < 0 ? v - 0.5 : v + 0.5);
+}
+
+__global__ void fill_image_kernel(uint8_t* img, uint64_t nchunks, uint32_t chunk_bytes) {
+    const uint64_t words_per_chunk = chunk_bytes / 4;
+    const uint64_t total = nchunks * words_per_chunk;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t w = i % words_per_chunk;
+        // codes -> 0, params -> (s=1, a=128) = 0x8001 per u16
+        reinterpret_cast<uint32_t*>(img)[i] = (w * 4 < kCodeBytes) ? 0u : 0x80018001u;
+    }
+}
+
+// Level 1 (quant.cpp:14-44): one CTA per row. Records the first non-finite
+// element (row-major linear index) in *bad via atomicMin.
+__global__ void quantize_level1_kernel(const float* __restrict__ w, int64_t ldw, uint32_t n,
+                                       uint32_t k, int8_t* __restrict__ q, float* __restrict__ cs,
+                                       unsigned long long* bad) {
+    const uint32_t row = blockIdx.x;
+    if (row >= n) return;
+    const float* wr = w + int64_t(row) * ldw;
+    float amax = 0.0f;
+    for (uint32_t j = threadIdx.x; j < k; j += blockDim.x) {
+        const float v = wr[j];
+        if (!isfinite(v)) atomicMin(bad, (unsigned long long)row * k + j);
+        amax = fmaxf(amax, fabsf(v));
+    }
+    __shared__ float red[32];
+    for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = amax;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float v = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.0f;
+        for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+        if (threadIdx.x == 0) red[0] = v;
+    }
+    __syncthreads();
+    amax = red[0];
+    const float s = amax == 0.0f ? 1.0f : __fdiv_rn(amax, 119.0f);
+    if (threadIdx.x == 0) cs[row] = s;
+    const double sd = double(s);
+    for (uint32_t j = threadIdx.x; j < k; j += blockDim.x) {
+        int v = round_half_away(__ddiv_rn(double(wr[j]), sd));
+        v = v < -119 ? -119 : (v > 119 ? 119 : v);
+        q[uint64_t(row) * k + j] = int8_t(v);
+    }
+}
+
+// Level 2 (quant.cpp:48-104) + device-image packing: one warp per
+// (row, group). Requires g % 32 == 0.
+__global__ void quantize_level2_pack_kernel(const int8_t* __restrict__ q, uint32_t n, uint32_t k,
+                                            uint32_t g, uint8_t* __restrict__ img,
+                                            uint32_t chunk_bytes, uint32_t KB, uint32_t P) {
+    const uint32_t gpr = k / g;
+    const uint64_t gw = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) / 32;
+    const uint32_t lane = threadIdx.x % 32;
+    if (gw >= uint64_t(n) * gpr) return;
+    const uint32_t row = static_cast<uint32_t>(gw / gpr), gi = static_cast<uint32_t>(gw % gpr);
+    const int8_t* qg = q + uint64_t(row) * k + uint64_t(gi) * g;
+    int mn = 127, mx = -128;
+    for (uint32_t j = lane; j < g; j += 32) {
+        const int v = qg[j];
+        mn = min(mn, v);
+        mx = max(mx, v);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    // group_params, quant.cpp:48-56
+    int s = round_half_away(__ddiv_rn(double(mx - mn), 15.0));
+    s = s < 1 ? 1 : s;
+    const uint32_t a = uint32_t(128 + mn);
+    // encode, quant.cpp:58-60; word = 8 codes, interleaved (packed.cpp:12-19)
+    for (uint32_t wi = lane; wi < g / 8; wi += 32) {
+        const uint32_t k0 = gi * g + wi * 8;
+        uint32_t c8[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            int c = round_half_away(__ddiv_rn(double(int(qg[wi * 8 + e]) - mn), double(s)));
+            c8[e] = uint32_t(c < 0 ? 0 : (c > 15 ? 15 : c));
+        }
+        uint32_t word = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) word |= (c8[j] | (c8[j + 4] << 4)) << (8 * j);
+        const uint32_t kb = k0 / kKBlock, c = (k0 % kKBlock) / 32, wsub = (k0 % 32) / 8;
+        *reinterpret_cast<uint32_t*>(img + code_offset(chunk_bytes, KB, row, kb, c) + wsub * 4) =
+            word;
+    }
+    // params for every 32-sub-block that starts a param region inside this group
+    const uint32_t sub_per_p = kSubBlocks / P;
+    for (uint32_t sb = lane; sb < g / 32; sb += 32) {
+        const uint32_t k0 = gi * g + sb * 32;
+        const uint32_t kb = k0 / kKBlock, c = (k0 % kKBlock) / 32;
+        if (c % sub_per_p == 0)
+            *reinterpret_cast<uint16_t*>(img + param_offset(chunk_bytes, KB, row, kb, c / sub_per_p)) =
+                uint16_t(uint32_t(s) | (a << 8));
+    }
+}
+
+// reconstruct_int8 through the mainloop's dequant (lqq_dequant_word): one
+// thread per (row, 32-element sub-block).
+__global__ void dequant_image_kernel(const uint8_t* __restrict__ img, uint32_t n, uint32_t k,
+                                     uint32_t chunk_bytes, uint32_t KB, uint32_t P,
+                                     int8_t* __restrict__ out, int64_t ldo) {
+    const uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    const uint32_t nsub = KB * kSubBlocks;
+    if (t >= uint64_t(n) * nsub) return;
+    const uint32_t row = static_cast<uint32_t>(t / nsub), sb = static_cast<uint32_t>(t % nsub);
+    const uint32_t kb = sb / kSubBlocks, c = sb % kSubBlocks;
+    const uint32_t sa = *reinterpret_cast<const uint16_t*>(
+        img + param_offset(chunk_bytes, KB, row, kb, c / (kSubBlocks / P)));
+    const uint4 v = *reinterpret_cast<const uint4*>(img + code_offset(chunk_bytes, KB, row, kb, c));
+    const uint32_t s = sa & 0xFFu, a4 = (sa >> 8) * 0x01010101u;
+    uint32_t o[8];
+    lqq_dequant_word(v.x, s, a4, o[0], o[1]);
+    lqq_dequant_word(v.y, s, a4, o[2], o[3]);
+    lqq_dequant_word(v.z, s, a4, o[4], o[5]);
+    lqq_dequant_word(v.w, s, a4, o[6], o[7]);
+    const uint32_t k0 = kb * kKBlock + c * 32;
+    int8_t* dst = out + int64_t(row) * ldo + k0;
+    if (k0 + 32 <= k && (reinterpret_cast<uintptr_t>(dst) % 16) == 0) {
+        uint4* d4 = reinterpret_cast<uint4*>(dst);
+        d4[0] = make_uint4(o[0], o[1], o[2], o[3]);
+        d4[1] = make_uint4(o[4], o[5], o[6], o[7]);
+    } else {
+        for (uint32_t e = 0; e < 32 && k0 + e < k; ++e) dst[e] = int8_t(o[e / 4] >> (8 * (e % 4)));
+    }
+}
+
+// Per-token activation quantization (gemm.cpp:19-47): one CTA per row.
+__global__ void quantize_activations_kernel(const float* __restrict__ x, int64_t ldx, uint32_t m,
+                                            uint32_t k, int8_t* __restrict__ q, int64_t ldq,
+                                            float* __restrict__ ts, unsigned long long* bad) {
+    const uint32_t row = blockIdx.x;
+    if (row >= m) return;
+    const float* xr = x + int64_t(row) * ldx;
+    float amax = 0.0f;
+    for (uint32_t j = threadIdx.x; j < k; j += blockDim.x) {
+        const float v = xr[j];
+        if (bad && !isfinite(v)) atomicMin(bad, (unsigned long long)row * k + j);
+        amax = fmaxf(amax, fabsf(v));
+    }
+    __shared__ float red[32];
+    for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = amax;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float v = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.0f;
+        for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+        if (threadIdx.x == 0) red[0] = v;
+    }
+    __syncthreads();
+    amax = red[0];
+    const float s = amax == 0.0f ? 1.0f : __fdiv_rn(amax, 127.0f);
+    if (threadIdx.x == 0) ts[row] = s;
+    const double sd = double(s);
+    for (uint32_t j = threadIdx.x; j < k; j += blockDim.x) {
+        int v = round_half_away(__ddiv_rn(double(xr[j]), sd));
+        v = v < -127 ? -127 : (v > 127 ? 127 : v);
+        q[int64_t(row) * ldq + j] = int8_t(v);
+    }
+}
+
+}  // namespace lqg

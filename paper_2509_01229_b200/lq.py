@@ -1,0 +1,409 @@
+"""Host-side mirror of the reference's ``namespace lq`` interface for the W4A8
+path, backed by the sm_100a kernels in liblqg.so.
+
+Same names, argument meaning and error behaviour as the reference
+(/root/reference/proj/include/lq/gemm.hpp:25-66, bundle.hpp:36-69,
+errors.hpp:15-28), so a caller of ``lq::gemm_w4a8_accum`` / ``lq::gemm_w4a8``
+can switch to this module and keep its tests. Every compute call runs on the
+GPU through the C ABI (include/lqg.h); there is no CPU fallback.
+
+Differences a caller can observe:
+  * ``TileConfig`` and ``Engine`` are validated with the reference rules but
+    do not change the computation (the reference contract makes results
+    independent of both, test_gemm.cpp:96-130).
+  * The device layout needs ``group_size % 32 == 0``; other group sizes raise
+    ``ValidationError`` at the first GEMM.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+
+
+# ---------------------------------------------------------------- errors
+class ValidationError(RuntimeError):
+    """lq::ValidationError (errors.hpp:15-17): bad input data."""
+
+
+class VerificationError(RuntimeError):
+    """lq::VerificationError (errors.hpp:19-21): a checked invariant failed."""
+
+
+class IoError(RuntimeError):
+    """lq::IoError (errors.hpp:23-28)."""
+
+    def __init__(self, msg: str, byte_offset: int = 0):
+        super().__init__(f"{msg} (byte offset {byte_offset})")
+        self.byte_offset = byte_offset
+
+
+class CudaError(RuntimeError):
+    """A CUDA runtime/driver failure inside liblqg (no reference analogue)."""
+
+
+class UnsupportedDeviceError(RuntimeError):
+    """No sm_100 device: liblqg has no CPU fallback."""
+
+
+_ERRORS = {1: ValidationError, 2: VerificationError, 3: IoError, 4: CudaError, 5: CudaError,
+           6: UnsupportedDeviceError}
+
+
+def check(rc: int) -> None:
+    if rc:
+        msg = _lib.lib().lqg_last_error().decode()
+        raise _ERRORS.get(rc, RuntimeError)(msg)
+
+
+# ---------------------------------------------------------------- types
+class WeightLayout(enum.IntEnum):
+    """bundle.hpp:36-39"""
+    PlainRowMajor = 0
+    DualMmaPacked = 1
+
+
+class Engine(enum.IntEnum):
+    """gemm.hpp:44"""
+    Scalar = 0
+    Packed = 1
+
+
+@dataclass
+class FragmentDescriptor:
+    """layout.hpp:33-46 (defaults = the Hopper dual-MMA geometry)."""
+    warps_per_group: int = 4
+    threads_per_warp: int = 32
+    mma_m: int = 64
+    mma_k: int = 32
+    elements_per_thread_per_mma: int = 16
+    dual_k_span: int = 64
+
+    def validate(self) -> None:
+        """layout.cpp:10-22"""
+        slab = self.mma_m * self.mma_k
+        per_group = self.warps_per_group * self.threads_per_warp * self.elements_per_thread_per_mma
+        if slab != per_group:
+            raise ValidationError(f"fragment descriptor mismatch: mma_m*mma_k = {slab} but group "
+                                  f"covers {per_group} elements")
+        if self.dual_k_span != 2 * self.mma_k:
+            raise ValidationError("dual_k_span must be 2*mma_k")
+        if 0 in (self.warps_per_group, self.threads_per_warp, self.mma_m, self.mma_k):
+            raise ValidationError("fragment descriptor has a zero field")
+
+
+@dataclass(eq=False)
+class QuantizedWeightBundle:
+    """bundle.hpp:41-69. Arrays are numpy: packed_weights u8 ((n*k+1)//2),
+    group_scales / group_offsets u8 (n*(k//group_size)), channel_scales f32 (n)."""
+    n: int = 0
+    k: int = 0
+    group_size: int = 64
+    layout: WeightLayout = WeightLayout.PlainRowMajor
+    fragment: FragmentDescriptor = field(default_factory=FragmentDescriptor)
+    packed_weights: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint8))
+    group_scales: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint8))
+    group_offsets: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint8))
+    channel_scales: np.ndarray = field(default_factory=lambda: np.zeros(0, np.float32))
+    _device: dict = field(default_factory=dict, repr=False, compare=False)
+
+    def groups_per_row(self) -> int:
+        return self.k // self.group_size
+
+    def scale_of(self, row: int, group: int) -> int:
+        return int(self.group_scales[row * self.groups_per_row() + group])
+
+    def offset_of(self, row: int, group: int) -> int:
+        return int(self.group_offsets[row * self.groups_per_row() + group])
+
+    def _view(self):
+        """Borrowed lqg_bundle_view; keeps the contiguous arrays alive."""
+        keep = [np.ascontiguousarray(self.packed_weights, np.uint8),
+                np.ascontiguousarray(self.group_scales, np.uint8),
+                np.ascontiguousarray(self.group_offsets, np.uint8),
+                np.ascontiguousarray(self.channel_scales, np.float32)]
+        f = self.fragment
+        v = _lib.BundleViewC(
+            self.n, self.k, self.group_size, int(self.layout),
+            _lib.FragmentDescriptorC(f.warps_per_group, f.threads_per_warp, f.mma_m, f.mma_k,
+                                     f.elements_per_thread_per_mma, f.dual_k_span),
+            keep[0].ctypes.data, keep[0].size, keep[1].ctypes.data, keep[2].ctypes.data,
+            keep[1].size,
+            keep[3].ctypes.data if keep[3].size == self.n else None)
+        return v, keep
+
+    def validate(self) -> None:
+        """bundle.cpp:89-135 (host-only, same rules and messages)."""
+        if self.group_scales.size != self.group_offsets.size:
+            raise ValidationError("group parameter arrays have wrong size")
+        v, _keep = self._view()
+        check(_lib.lib().lqg_bundle_validate(C.byref(v)))
+
+    def device_weights(self, device: int = 0) -> "DeviceWeights":
+        """The prepacked device copy (created on first use, then cached)."""
+        dw = self._device.get(device)
+        if dw is None:
+            dw = DeviceWeights.from_bundle(self, device)
+            self._device[device] = dw
+        return dw
+
+
+@dataclass
+class TileConfig:
+    """gemm.hpp:29-33. Validated with the reference rules (gemm.cpp:11-17); the
+    device kernel picks its own tiles (results are tile-independent)."""
+    m_t: int = 64
+    n_t: int = 64
+    k_t: int = 64
+
+    def validate(self, b: QuantizedWeightBundle) -> None:
+        if self.m_t < 1 or self.n_t < 1 or self.k_t < 1:
+            raise ValidationError("tile extents must be >= 1")
+        if b.layout == WeightLayout.DualMmaPacked and self.k_t % b.fragment.dual_k_span != 0:
+            raise ValidationError(f"k_t must be a multiple of {b.fragment.dual_k_span} when "
+                                  "consuming the dual-MMA layout")
+
+
+@dataclass
+class ActivationQuant:
+    """gemm.hpp:35-39: values m*k int8 codes in [-127, 127], token_scales m."""
+    m: int = 0
+    k: int = 0
+    values: np.ndarray = field(default_factory=lambda: np.zeros(0, np.int8))
+    token_scales: np.ndarray = field(default_factory=lambda: np.zeros(0, np.float32))
+
+
+@dataclass
+class GemmShape:
+    """gemm.hpp:25-27"""
+    m: int = 0
+    n: int = 0
+    k: int = 0
+
+
+# ---------------------------------------------------------------- entry points
+def quantize_activations_per_token(x, m: int, k: int) -> ActivationQuant:
+    """gemm.cpp:19-47, computed by the lqg activation-quant kernel (bit-exact)."""
+    import torch
+    if m < 1 or k < 1:
+        raise ValidationError("activation dimensions must be >= 1")
+    xa = np.ascontiguousarray(np.asarray(x, dtype=np.float32)).reshape(-1)
+    if xa.size != m * k:
+        raise ValidationError("activation buffer size does not match m*k")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    xd = torch.from_numpy(xa).to(dev).view(m, k)
+    q, ts = quantize_activations(xd, check_finite=True)
+    return ActivationQuant(m, k, q.cpu().numpy().reshape(-1), ts.cpu().numpy())
+
+
+def _prepare(act: ActivationQuant, weights: QuantizedWeightBundle, tile: TileConfig,
+             engine: Engine):
+    # gemm.cpp:141-146 and 151-158, in the reference's order
+    weights.validate()
+    tile.validate(weights)
+    if act.k != weights.k:
+        raise ValidationError(f"activation depth {act.k} does not match weight depth {weights.k}")
+    if act.k * 127 * 127 >= (1 << 31):
+        raise ValidationError(f"k = {act.k} risks 32-bit accumulator overflow (k*127*127 >= 2^31)")
+    if Engine(engine) == Engine.Packed and tile.k_t % weights.fragment.dual_k_span != 0:
+        raise ValidationError(f"k_t must be a multiple of {weights.fragment.dual_k_span} for the "
+                              "packed engine")
+    vals = np.ascontiguousarray(np.asarray(act.values, dtype=np.int8)).reshape(-1)
+    if vals.size != act.m * act.k or act.m < 1:
+        raise ValidationError("activation buffer size does not match m*k")
+    ts = np.ascontiguousarray(np.asarray(act.token_scales, dtype=np.float32)).reshape(-1)
+    import torch
+    dw = weights.device_weights(torch.cuda.current_device())
+    return dw, vals, ts
+
+
+def gemm_w4a8_accum(act: ActivationQuant, weights: QuantizedWeightBundle,
+                    tile: TileConfig = TileConfig(), engine: Engine = Engine.Packed) -> np.ndarray:
+    """gemm.hpp:49-51: INT32 accumulators, row-major m*n (1-D, like the
+    reference's std::vector)."""
+    dw, vals, _ts = _prepare(act, weights, tile, engine)
+    acc = np.empty(act.m * weights.n, np.int32)
+    check(_lib.lib().lqg_gemm_w4a8_accum_host(dw.handle, vals.ctypes.data, act.m, acc.ctypes.data,
+                                              None))
+    return acc
+
+
+def gemm_w4a8(act: ActivationQuant, weights: QuantizedWeightBundle,
+              tile: TileConfig = TileConfig(), engine: Engine = Engine.Packed) -> np.ndarray:
+    """gemm.hpp:54-55: float outputs, row-major m*n, bit-identical to the
+    reference epilogue (quant.cpp:125-127)."""
+    dw, vals, ts = _prepare(act, weights, tile, engine)
+    if ts.size != act.m:
+        raise ValidationError("token scale array has wrong size")
+    y = np.empty(act.m * weights.n, np.float32)
+    check(_lib.lib().lqg_gemm_w4a8_host(dw.handle, vals.ctypes.data, ts.ctypes.data, act.m,
+                                        y.ctypes.data, 0, None))
+    return y
+
+
+# ---------------------------------------------------------------- device API
+Y_DTYPES = {"float32": 0, "float16": 1, "bfloat16": 2}
+
+
+def _y_code(dtype) -> int:
+    name = str(dtype).replace("torch.", "")
+    if name not in Y_DTYPES:
+        raise ValidationError(f"unsupported output dtype {dtype}")
+    return Y_DTYPES[name]
+
+
+def _stream_ptr(stream):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+class Workspace:
+    """lqg_workspace: a split-K scratch per concurrent stream."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        check(_lib.lib().lqg_workspace_create(device, C.byref(h)))
+        self.handle, self.device = h, device
+
+    def close(self):
+        if self.handle:
+            _lib.lib().lqg_workspace_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class DeviceWeights:
+    """A device-resident, prepacked W4 weight handle (lqg_weights)."""
+
+    def __init__(self, handle: C.c_void_p, device: int):
+        self.handle, self.device = handle, device
+        n, k, g = C.c_uint32(), C.c_uint32(), C.c_uint32()
+        check(_lib.lib().lqg_weights_shape(handle, C.byref(n), C.byref(k), C.byref(g)))
+        self.n, self.k, self.group_size = n.value, k.value, g.value
+
+    @classmethod
+    def from_bundle(cls, b: QuantizedWeightBundle, device: int = 0) -> "DeviceWeights":
+        if b.group_scales.size != b.group_offsets.size:
+            raise ValidationError("group parameter arrays have wrong size")
+        v, _keep = b._view()
+        h = C.c_void_p()
+        check(_lib.lib().lqg_weights_create(C.byref(v), device, C.byref(h)))
+        return cls(h, device)
+
+    @classmethod
+    def quantize(cls, w, group_size: int, stream=None) -> "DeviceWeights":
+        """Two-level LiquidQuant of device FP32 weights [n, k] on the GPU
+        (build_bundle, quant.cpp:203-232, bit-exact)."""
+        import torch
+        if not (w.is_cuda and w.dtype == torch.float32 and w.dim() == 2 and w.stride(1) == 1):
+            raise ValidationError("weights must be a row-major CUDA float32 [n, k] tensor")
+        h = C.c_void_p()
+        check(_lib.lib().lqg_weights_quantize(w.data_ptr(), w.stride(0), w.shape[0], w.shape[1],
+                                              group_size, _stream_ptr(stream), C.byref(h)))
+        return cls(h, w.device.index)
+
+    @property
+    def device_bytes(self) -> int:
+        return int(_lib.lib().lqg_weights_device_bytes(self.handle))
+
+    def _check_x(self, xq):
+        import torch
+        if not (xq.is_cuda and xq.dtype == torch.int8 and xq.dim() == 2 and xq.shape[1] == self.k
+                and xq.stride(1) == 1):
+            raise ValidationError(f"activations must be a CUDA int8 [m, {self.k}] row-major tensor")
+
+    def gemm(self, xq, ts, out=None, out_dtype=None, workspace: Workspace | None = None,
+             stream=None):
+        """Y[m, n] = (X_i8 @ W^_i8.T) * cs[n] * ts[m] in out_dtype (default bf16)."""
+        import torch
+        self._check_x(xq)
+        m = xq.shape[0]
+        if out is None:
+            out = torch.empty(m, self.n, dtype=out_dtype or torch.bfloat16, device=xq.device)
+        check(_lib.lib().lqg_gemm_w4a8(
+            self.handle, xq.data_ptr(), xq.stride(0), ts.data_ptr(), m, out.data_ptr(),
+            out.stride(0), _y_code(out.dtype), workspace.handle if workspace else None,
+            _stream_ptr(stream)))
+        return out
+
+    def gemm_accum(self, xq, out=None, workspace: Workspace | None = None, stream=None):
+        import torch
+        self._check_x(xq)
+        m = xq.shape[0]
+        if out is None:
+            out = torch.empty(m, self.n, dtype=torch.int32, device=xq.device)
+        check(_lib.lib().lqg_gemm_w4a8_accum(
+            self.handle, xq.data_ptr(), xq.stride(0), m, out.data_ptr(), out.stride(0),
+            workspace.handle if workspace else None, _stream_ptr(stream)))
+        return out
+
+    def gemm_host(self, x_host, ts_host, y_host, stream=None) -> None:
+        """The reference-facing host-buffer call (lqg_gemm_w4a8_host): inputs
+        and output live in host memory (pinned for full PCIe speed)."""
+        import torch
+        m = x_host.shape[0]
+        check(_lib.lib().lqg_gemm_w4a8_host(self.handle, x_host.data_ptr(), ts_host.data_ptr(), m,
+                                            y_host.data_ptr(), _y_code(y_host.dtype),
+                                            _stream_ptr(stream)))
+
+    def dequant(self, out=None, stream=None):
+        """W^ as INT8 [n, k] through the mainloop's LQQ routine."""
+        import torch
+        if out is None:
+            out = torch.empty(self.n, self.k, dtype=torch.int8, device=f"cuda:{self.device}")
+        check(_lib.lib().lqg_dequant_weights(self.handle, out.data_ptr(), out.stride(0),
+                                             _stream_ptr(stream)))
+        return out
+
+    def export(self) -> QuantizedWeightBundle:
+        """Plain-layout host bundle of this handle."""
+        n, k, g = self.n, self.k, self.group_size
+        packed = np.zeros((n * k + 1) // 2, np.uint8)
+        sc = np.zeros(n * (k // g), np.uint8)
+        of = np.zeros(n * (k // g), np.uint8)
+        cs = np.zeros(n, np.float32)
+        check(_lib.lib().lqg_weights_export(self.handle, packed.ctypes.data, sc.ctypes.data,
+                                            of.ctypes.data, cs.ctypes.data))
+        return QuantizedWeightBundle(n, k, g, WeightLayout.PlainRowMajor, FragmentDescriptor(),
+                                     packed, sc, of, cs)
+
+    def close(self):
+        if self.handle:
+            _lib.lib().lqg_weights_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def quantize_activations(x, out_q=None, out_ts=None, check_finite: bool = False, stream=None):
+    """Per-token INT8 quantization of a CUDA float32 [m, k] tensor
+    (gemm.cpp:19-47, bit-exact). Returns (q int8 [m, k], ts float32 [m])."""
+    import torch
+    if not (x.is_cuda and x.dtype == torch.float32 and x.dim() == 2 and x.stride(1) == 1):
+        raise ValidationError("activations must be a row-major CUDA float32 [m, k] tensor")
+    m, k = x.shape
+    q = out_q if out_q is not None else torch.empty(m, k, dtype=torch.int8, device=x.device)
+    ts = out_ts if out_ts is not None else torch.empty(m, dtype=torch.float32, device=x.device)
+    check(_lib.lib().lqg_quantize_activations(x.data_ptr(), x.stride(0), m, k, q.data_ptr(),
+                                              q.stride(0), ts.data_ptr(), int(check_finite),
+                                              _stream_ptr(stream)))
+    return q, ts
+
+
+def launch_count() -> int:
+    """Kernels launched by liblqg.so in this process."""
+    return int(_lib.lib().lqg_kernel_launch_count())
