@@ -8,6 +8,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -306,8 +307,18 @@ int alloc_weights(int dev, const ImageGeom& G, lqg_weights** out) {
     return LQG_OK;
 }
 
+// Token tile: <= 192 so that the INT32 accumulator stays double-buffered in
+// TMEM (2 x 192 columns + a 2-slot A ring, see tmem_plan).
+constexpr uint32_t kMaxTileM = 192;
+
+uint32_t env_u32(const char* name, uint32_t dflt) {
+    const char* v = std::getenv(name);
+    return v && *v ? static_cast<uint32_t>(std::strtoul(v, nullptr, 10)) : dflt;
+}
+
 uint32_t choose_bn(uint32_t m, uint32_t* mt) {
-    const uint32_t MT = (m + 255) / 256;
+    static const uint32_t cap = env_u32("LQG_DEBUG_MAX_BN", kMaxTileM);
+    const uint32_t MT = (m + cap - 1) / cap;
     const uint32_t per = (m + MT - 1) / MT;
     *mt = MT;
     return std::max(16u, (per + 15) / 16 * 16);
@@ -339,7 +350,7 @@ int launch_gemm(const lqg_weights* w, const int8_t* d_x, int64_t ldx, const floa
     CUtensorMap tmap;
     const cuuint64_t dims[2] = {G.k, m};
     const cuuint64_t strides[1] = {cuuint64_t(ldx)};
-    const cuuint32_t box[2] = {kKBlock, BN};
+    const cuuint32_t box[2] = {kXAtom, BN};
     const cuuint32_t estr[2] = {1, 1};
     CUresult cr = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(d_x), dims,
                       strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -368,10 +379,13 @@ int launch_gemm(const lqg_weights* w, const int8_t* d_x, int64_t ldx, const floa
     p.stage_bytes = (BN * kKBlock + G.chunk_bytes + 1023) / 1024 * 1024;
     const uint32_t budget = 227 * 1024 - 2048;
     p.stages = std::min<uint32_t>(kMaxStages, budget / p.stage_bytes);
+    if (uint32_t st = env_u32("LQG_DEBUG_STAGES", 0)) p.stages = std::min(p.stages, st);
     if (p.stages < 2) return set_err(LQG_EVALIDATION, "tile configuration does not fit shared memory");
     p.total_iters = uint64_t(MT) * G.NT * G.KB;
-    const uint32_t grid = static_cast<uint32_t>(
+    uint32_t grid = static_cast<uint32_t>(
         std::min<uint64_t>(std::min<uint32_t>(w->num_sms, kMaxSlots), p.total_iters));
+    if (uint32_t gd = env_u32("LQG_DEBUG_GRID", 0))
+        grid = static_cast<uint32_t>(std::min<uint64_t>({gd, uint64_t(kMaxSlots), p.total_iters}));
     const size_t smem = size_t(p.stages) * p.stage_bytes + 1024 + 1024;
 
     DeviceGuard dg(w->device);

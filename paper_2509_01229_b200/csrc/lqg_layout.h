@@ -6,14 +6,14 @@
 // 1-D bulk TMA copy per (weight tile, k-block) and for one TMEM lane per
 // weight row in the dequant warps:
 //
-//   tile  = 128 weight rows (the tcgen05 M), k-block = 128 reduction elements
+//   tile  = 128 weight rows (the tcgen05 M), k-block = 256 reduction elements
 //   chunk(nt, kb) at byte ((nt * KB) + kb) * chunk_bytes, tile-major so a CTA
 //   streaming one tile's k-blocks reads contiguous HBM.
 //
-//   chunk = codes [4 sub-blocks c][128 rows r][16 B]      8192 B
-//         + params [P][128 rows] u16 (lo byte s_u8, hi byte a)   256*P B
+//   chunk = codes [8 sub-blocks c][128 rows r][16 B]                 16384 B
+//         + params [P][128 rows] u16 (lo byte s_u8, hi byte a)       256*P B
 //
-//   codes(c, r) holds the 32 UINT4 codes of row r, k = kb*128 + 32c + 0..31,
+//   codes(c, r) holds the 32 UINT4 codes of row r, k = kb*256 + 32c + 0..31,
 //   as four little-endian words; word w carries k-offsets 8w..8w+7 with the
 //   reference register interleave (packed.cpp:12-19): element 8w+j in the
 //   low nibble and 8w+j+4 in the high nibble of byte j. One LDS.128 per
@@ -21,8 +21,9 @@
 //   After LQQ dequant, word w yields TMEM columns 2w (lo) and 2w+1 (hi) of
 //   sub-block c, i.e. the K-major int8 A operand of tcgen05.mma kind::i8.
 //
-//   P = params per k-block: 1 if g % 128 == 0, 2 if g % 64 == 0, else 4
-//   (g % 32 == 0 required). Param p covers sub-blocks [p*4/P, (p+1)*4/P).
+//   P = params per k-block: 1 if g % 256 == 0, 2 if g % 128 == 0,
+//   4 if g % 64 == 0, else 8 (g % 32 == 0 required). Param p covers
+//   sub-blocks [p*8/P, (p+1)*8/P).
 //   Padding rows (n >= N) and padding k (k >= K) carry code 0 with s=1,
 //   a=128, which dequantizes to exactly 0.
 #pragma once
@@ -35,10 +36,11 @@
 
 namespace lqg {
 
-constexpr uint32_t kTileN = 128;          // weight rows per tile (tcgen05 M)
-constexpr uint32_t kKBlock = 128;         // reduction elements per k-block
-constexpr uint32_t kCodeBytes = kTileN * kKBlock / 2;  // 8192
-constexpr uint32_t kSubBlocks = 4;        // 32-element sub-blocks per k-block
+constexpr uint32_t kTileN = 128;                       // weight rows per tile (tcgen05 M)
+constexpr uint32_t kKBlock = 256;                      // reduction elements per k-block
+constexpr uint32_t kSubBlocks = kKBlock / 32;          // 32-element sub-blocks per k-block
+constexpr uint32_t kCodeBytes = kTileN * kKBlock / 2;  // 16384
+constexpr uint32_t kXAtom = 128;                       // bytes of K per SW128 activation box
 
 struct ImageGeom {
     uint32_t n, k, g;
@@ -47,9 +49,15 @@ struct ImageGeom {
 };
 
 inline uint32_t params_per_kblock(uint32_t g) {
-    if (g % 128 == 0) return 1;
-    if (g % 64 == 0) return 2;
-    return 4;
+    if (g % 256 == 0) return 1;
+    if (g % 128 == 0) return 2;
+    if (g % 64 == 0) return 4;
+    return 8;
+}
+
+// log2(sub-blocks per param): sub-block c uses param c >> shift.
+__host__ __device__ inline uint32_t param_shift(uint32_t P) {
+    return P == 1 ? 3u : (P == 2 ? 2u : (P == 4 ? 1u : 0u));
 }
 
 inline ImageGeom make_geom(uint32_t n, uint32_t k, uint32_t g) {
