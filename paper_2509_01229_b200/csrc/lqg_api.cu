@@ -310,6 +310,8 @@ int alloc_weights(int dev, const ImageGeom& G, lqg_weights** out) {
 // Token tile: <= 192 so that the INT32 accumulator stays double-buffered in
 // TMEM (2 x 192 columns + a 2-slot A ring, see tmem_plan).
 constexpr uint32_t kMaxTileM = 192;
+// Token tiles up to this size run in decode mode (see launch_gemm).
+constexpr uint32_t kDecodeMaxBN = 64;
 
 uint32_t env_u32(const char* name, uint32_t dflt) {
     const char* v = std::getenv(name);
@@ -377,16 +379,25 @@ int launch_gemm(const lqg_weights* w, const int8_t* d_x, int64_t ldx, const floa
     p.chunk_bytes = G.chunk_bytes;
     p.out_kind = out_kind;
     p.stage_bytes = (BN * kKBlock + G.chunk_bytes + 1023) / 1024 * 1024;
-    const uint32_t budget = 227 * 1024 - 2048;
+    // Decode mode (small token tiles): <= 110 KB of shared memory and 256 TMEM
+    // columns, so two CTAs fit on an SM and the next GEMM in the stream (PDL)
+    // can stream its weights while this one drains. Otherwise one CTA per SM.
+    const bool decode = BN <= kDecodeMaxBN && !env_u32("LQG_DEBUG_NO_DECODE_MODE", 0);
+    p.tmem_cols = decode ? 256 : 512;
+    // ~24 MB of weights across the grid (enough to cover a kernel tail at HBM rate).
+    p.l2_prefetch = env_u32("LQG_L2_PREFETCH_CHUNKS", decode ? 10 : 0);
+    const uint32_t budget = decode ? 110 * 1024 - 3072 : 227 * 1024 - 3072;
     p.stages = std::min<uint32_t>(kMaxStages, budget / p.stage_bytes);
     if (uint32_t st = env_u32("LQG_DEBUG_STAGES", 0)) p.stages = std::min(p.stages, st);
     if (p.stages < 2) return set_err(LQG_EVALIDATION, "tile configuration does not fit shared memory");
+    if (tmem_plan(BN, p.tmem_cols).a_slots < 1)
+        return set_err(LQG_EVALIDATION, "tile configuration does not fit tensor memory");
     p.total_iters = uint64_t(MT) * G.NT * G.KB;
     uint32_t grid = static_cast<uint32_t>(
         std::min<uint64_t>(std::min<uint32_t>(w->num_sms, kMaxSlots), p.total_iters));
     if (uint32_t gd = env_u32("LQG_DEBUG_GRID", 0))
         grid = static_cast<uint32_t>(std::min<uint64_t>({gd, uint64_t(kMaxSlots), p.total_iters}));
-    const size_t smem = size_t(p.stages) * p.stage_bytes + 1024 + 1024;
+    const size_t smem = size_t(p.stages) * p.stage_bytes + 1024 + 2048;
 
     DeviceGuard dg(w->device);
     cudaError_t e = cudaSuccess;
@@ -395,7 +406,17 @@ int launch_gemm(const lqg_weights* w, const int8_t* d_x, int64_t ldx, const floa
                                  227 * 1024);
     });
     if (e != cudaSuccess) return set_err(LQG_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
-    lqg_w4a8_gemm_kernel<<<grid, kThreads, smem, stream>>>(tmap, p);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = env_u32("LQG_DEBUG_NO_PDL", 0) ? 0 : 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel, tmap, p));
     g_launches.fetch_add(1, std::memory_order_relaxed);
     LQG_CUDA(cudaGetLastError());
     return LQG_OK;
@@ -427,6 +448,16 @@ int out_kind_of(int y_dtype, uint32_t* kind) {
 extern "C" {
 
 const char* lqg_last_error(void) { return g_err.c_str(); }
+
+#ifdef LQG_TRACE
+// Debug build only: copy the per-CTA %globaltimer trace (160 x 16 u64).
+int lqg_debug_trace(unsigned long long* out) {
+    return cudaMemcpyFromSymbol(out, g_lqg_trace, sizeof(unsigned long long) * 160 * 16) ==
+                   cudaSuccess
+               ? 0
+               : 4;
+}
+#endif
 const char* lqg_version(void) { return "lqg 0.1 (sm_100a, tcgen05 kind::i8, TMEM-A LiquidQuant mainloop)"; }
 uint64_t lqg_kernel_launch_count(void) { return g_launches.load(); }
 

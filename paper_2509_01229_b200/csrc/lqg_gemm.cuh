@@ -53,21 +53,22 @@ enum OutKind : uint32_t { kOutAcc = 0, kOutF32 = 1, kOutF16 = 2, kOutBF16 = 3 };
 
 constexpr uint32_t kThreads = 512;
 constexpr uint32_t kMaxStages = 16;
-constexpr uint32_t kMaxASlots = 4;
+constexpr uint32_t kMaxASlots = 8;
 constexpr uint32_t kACols = kKBlock / 4;   // TMEM columns per A slot (4 int8 per column)
-constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kMaxBN = 256;
 
 struct TmemPlan {
     uint32_t acc_stride, acc_stages, a_base, a_slots;
 };
 
-__host__ __device__ inline TmemPlan tmem_plan(uint32_t BN) {
+// cols = allocated TMEM columns: 512 (one CTA per SM) or 256 (decode mode:
+// two co-resident CTAs, e.g. consecutive GEMMs overlapped by PDL).
+__host__ __device__ inline TmemPlan tmem_plan(uint32_t BN, uint32_t cols) {
     TmemPlan t;
     t.acc_stride = (BN + 31) / 32 * 32;
-    t.acc_stages = (2 * t.acc_stride + 2 * kACols <= kTmemCols) ? 2u : 1u;
+    t.acc_stages = (2 * t.acc_stride + 2 * kACols <= cols) ? 2u : 1u;
     t.a_base = (t.acc_stages * t.acc_stride + kACols - 1) / kACols * kACols;
-    t.a_slots = (kTmemCols - t.a_base) / kACols;
+    t.a_slots = (cols - t.a_base) / kACols;
     if (t.a_slots > kMaxASlots) t.a_slots = kMaxASlots;
     return t;
 }
@@ -88,6 +89,8 @@ struct GemmParams {
     uint32_t stages;           // shared-memory ring depth
     uint32_t stage_bytes;      // bytes per ring slot (X tile first, then W chunk)
     uint32_t out_kind;         // OutKind
+    uint32_t tmem_cols;        // 256 (decode mode) or 512
+    uint32_t l2_prefetch;      // weight chunks prefetched into L2 before the PDL wait
     uint64_t total_iters;      // MT*NT*KB
 };
 
@@ -135,7 +138,19 @@ __device__ __forceinline__ void store_out(const GemmParams& p, uint32_t m, uint3
         static_cast<__nv_bfloat16*>(p.out)[idx] = __float2bfloat16_rn(y);
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
+#ifdef LQG_TRACE
+__device__ unsigned long long g_lqg_trace[160 * 16];
+__device__ __forceinline__ void trace(uint32_t e) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_lqg_trace[blockIdx.x * 16 + e] = t;
+}
+#define LQG_T(e) trace(e)
+#else
+#define LQG_T(e) ((void)0)
+#endif
+
+__global__ void __launch_bounds__(kThreads, 2)
     lqg_w4a8_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const GemmParams p) {
     extern __shared__ uint8_t smem_raw[];
     // 1024-byte alignment for the SW128 activation tiles.
@@ -148,19 +163,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t ring_bytes = S * p.stage_bytes;
     // barriers after the ring
     const uint32_t bar_base = smem_base + ring_bytes;
-    auto full_bar = [&](uint32_t s) { return bar_base + 8 * s; };
-    auto empty_bar = [&](uint32_t s) { return bar_base + 8 * (kMaxStages + s); };
-    auto afull_bar = [&](uint32_t a) { return bar_base + 8 * (2 * kMaxStages + a); };
-    auto aempty_bar = [&](uint32_t a) { return bar_base + 8 * (2 * kMaxStages + kMaxASlots + a); };
-    auto accfull_bar = [&](uint32_t a) {
-        return bar_base + 8 * (2 * kMaxStages + 2 * kMaxASlots + a);
-    };
-    auto accempty_bar = [&](uint32_t a) {
-        return bar_base + 8 * (2 * kMaxStages + 2 * kMaxASlots + 2 + a);
-    };
-    uint8_t* misc = smem + ring_bytes + 8 * (2 * kMaxStages + 2 * kMaxASlots + 4);
+    auto wfull_bar = [&](uint32_t s) { return bar_base + 8 * s; };
+    auto xfull_bar = [&](uint32_t s) { return bar_base + 8 * (kMaxStages + s); };
+    auto empty_bar = [&](uint32_t s) { return bar_base + 8 * (2 * kMaxStages + s); };
+    constexpr uint32_t kB = 3 * kMaxStages;
+    auto afull_bar = [&](uint32_t a) { return bar_base + 8 * (kB + a); };
+    auto aempty_bar = [&](uint32_t a) { return bar_base + 8 * (kB + kMaxASlots + a); };
+    auto accfull_bar = [&](uint32_t a) { return bar_base + 8 * (kB + 2 * kMaxASlots + a); };
+    auto accempty_bar = [&](uint32_t a) { return bar_base + 8 * (kB + 2 * kMaxASlots + 2 + a); };
+    uint8_t* misc = smem + ring_bytes + 8 * (kB + 2 * kMaxASlots + 4);
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(misc);
     volatile uint32_t* epi_flag = reinterpret_cast<volatile uint32_t*>(misc + 16);
+    float* ts_s = reinterpret_cast<float*>(misc + 64);  // kMaxBN token scales
 
     const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const uint32_t G = gridDim.x;
@@ -168,12 +182,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint64_t end = cta_range_begin(blockIdx.x + 1, G, p.total_iters);
     const uint32_t n_local = static_cast<uint32_t>(end - beg);
     const uint32_t KB = p.KB;
-    const TmemPlan tp = tmem_plan(p.BN);
+    const TmemPlan tp = tmem_plan(p.BN, p.tmem_cols);
     const uint32_t x_bytes = p.BN * kKBlock;  // activation tile bytes per stage
 
+    if (threadIdx.x == 0) LQG_T(0);
     if (threadIdx.x == 0) {
         for (uint32_t s = 0; s < S; ++s) {
-            ptx::mbar_init(full_bar(s), 1);
+            ptx::mbar_init(wfull_bar(s), 1);
+            ptx::mbar_init(xfull_bar(s), 1);
             ptx::mbar_init(empty_bar(s), 1);
         }
         for (uint32_t a = 0; a < kMaxASlots; ++a) {
@@ -187,46 +203,111 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::fence_mbar_init();
     }
     if (warp == 0 && lane == 0) ptx::prefetch_tmap(&tmap_x);
-    if (warp == 2) ptx::tmem_alloc(ptx::smem_u32(tmem_holder), kTmemCols);
+    if (warp == 2) ptx::tmem_alloc(ptx::smem_u32(tmem_holder), p.tmem_cols);
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
+    // PDL: let the next kernel in the stream start its prologue and weight
+    // prefetch now; everything that reads or writes dependent memory below
+    // (activations, token scales, outputs, workspace) sits behind
+    // griddepcontrol.wait.
+    if (threadIdx.x == 0) ptx::launch_dependents();
+    if (threadIdx.x == 0) LQG_T(1);
 
     if (warp == 0) {
         // ------------------------------------------------------------ producer
-        const uint64_t pol_w = ptx::policy_evict_first();
+        // Weights (static) are streamed immediately: the first min(S, n)
+        // chunks are in flight before griddepcontrol.wait, so the weight
+        // stream of this GEMM overlaps the tail of the previous kernel.
+        // Activation tiles follow the dependency wait.
+        const uint64_t pol_w = p.MT == 1 ? ptx::policy_evict_first() : ptx::policy_evict_last();
         const uint64_t pol_x = ptx::policy_evict_last();
-        const uint32_t tx_bytes = x_bytes + p.chunk_bytes;
         const uint32_t atom_bytes = p.BN * kXAtom;
-        // incremental (tile, kb) walk: no divisions in the loop
         const uint64_t tile0 = beg / KB;
-        uint32_t kb = static_cast<uint32_t>(beg - tile0 * KB);
-        uint32_t mt = static_cast<uint32_t>(tile0 / p.NT);
-        uint32_t nt = static_cast<uint32_t>(tile0 - uint64_t(mt) * p.NT);
-        const uint8_t* src = p.wimg + (uint64_t(nt) * KB + kb) * p.chunk_bytes;
-        uint32_t s = 0, ph = 0;
-        for (uint32_t i = 0; i < n_local; ++i) {
-            ptx::mbar_wait(empty_bar(s), ph ^ 1);
-            if (ptx::elect_one()) {
-                const uint32_t slot = smem_base + s * p.stage_bytes;
-                ptx::mbar_arrive_expect_tx(full_bar(s), tx_bytes);
-                const int32_t k0 = int32_t(kb * kKBlock), m0 = int32_t(mt * p.BN);
-                ptx::tma_2d_g2s(slot, &tmap_x, k0, m0, full_bar(s), pol_x);
-                ptx::tma_2d_g2s(slot + atom_bytes, &tmap_x, k0 + int32_t(kXAtom), m0, full_bar(s),
-                                pol_x);
-                ptx::bulk_g2s(slot + x_bytes, src, p.chunk_bytes, full_bar(s), pol_w);
-            }
-            __syncwarp();
+        const uint32_t kb_0 = static_cast<uint32_t>(beg - tile0 * KB);
+        const uint32_t mt_0 = static_cast<uint32_t>(tile0 / p.NT);
+        const uint32_t nt_0 = static_cast<uint32_t>(tile0 - uint64_t(mt_0) * p.NT);
+        // weight walker
+        uint32_t wkb = kb_0, wnt = nt_0;
+        const uint8_t* src = p.wimg + (uint64_t(nt_0) * KB + kb_0) * p.chunk_bytes;
+        auto w_next = [&]() {
             src += p.chunk_bytes;
-            if (++kb == KB) {
-                kb = 0;
-                if (++nt == p.NT) {
-                    nt = 0;
-                    ++mt;
+            if (++wkb == KB) {
+                wkb = 0;
+                if (++wnt == p.NT) {
+                    wnt = 0;
                     src = p.wimg;
                 }
             }
+        };
+        // activation walker
+        uint32_t xkb = kb_0, xnt = nt_0, xmt = mt_0;
+        auto x_issue = [&](uint32_t st) {
+            const uint32_t slot = smem_base + st * p.stage_bytes;
+            ptx::mbar_arrive_expect_tx(xfull_bar(st), x_bytes);
+            const int32_t k0 = int32_t(xkb * kKBlock), m0 = int32_t(xmt * p.BN);
+            ptx::tma_2d_g2s(slot, &tmap_x, k0, m0, xfull_bar(st), pol_x);
+            ptx::tma_2d_g2s(slot + atom_bytes, &tmap_x, k0 + int32_t(kXAtom), m0, xfull_bar(st),
+                            pol_x);
+        };
+        auto x_next = [&]() {
+            if (++xkb == KB) {
+                xkb = 0;
+                if (++xnt == p.NT) {
+                    xnt = 0;
+                    ++xmt;
+                }
+            }
+        };
+        const uint32_t pre = n_local < S ? n_local : S;
+        for (uint32_t i = 0; i < pre; ++i) {
+            if (ptx::elect_one()) {
+                ptx::mbar_arrive_expect_tx(wfull_bar(i), p.chunk_bytes);
+                ptx::bulk_g2s(smem_base + i * p.stage_bytes + x_bytes, src, p.chunk_bytes,
+                              wfull_bar(i), pol_w);
+            }
+            __syncwarp();
+            w_next();
+        }
+        // Warm L2 with the next weight chunks too (no shared memory needed), so
+        // HBM keeps streaming this GEMM's weights while the previous kernel drains.
+        if (p.l2_prefetch > 0 && ptx::elect_one()) {
+            uint32_t pkb = wkb, pnt = wnt;
+            const uint8_t* psrc = src;
+            const uint32_t npf = min(p.l2_prefetch, n_local - pre);
+            for (uint32_t i = 0; i < npf; ++i) {
+                ptx::prefetch_l2(psrc, p.chunk_bytes);
+                psrc += p.chunk_bytes;
+                if (++pkb == KB) {
+                    pkb = 0;
+                    if (++pnt == p.NT) {
+                        pnt = 0;
+                        psrc = p.wimg;
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        ptx::griddep_wait();
+        if (lane == 0) LQG_T(2);
+        for (uint32_t i = 0; i < pre; ++i) {
+            if (ptx::elect_one()) x_issue(i);
+            __syncwarp();
+            x_next();
+        }
+        uint32_t s = pre == S ? 0 : pre, ph = pre == S ? 1 : 0;
+        for (uint32_t i = pre; i < n_local; ++i) {
+            ptx::mbar_wait(empty_bar(s), ph ^ 1);
+            if (ptx::elect_one()) {
+                ptx::mbar_arrive_expect_tx(wfull_bar(s), p.chunk_bytes);
+                ptx::bulk_g2s(smem_base + s * p.stage_bytes + x_bytes, src, p.chunk_bytes,
+                              wfull_bar(s), pol_w);
+                x_issue(s);
+            }
+            __syncwarp();
+            w_next();
+            x_next();
             if (++s == S) {
                 s = 0;
                 ph ^= 1;
@@ -234,19 +315,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
-        // The dequant warps wait on full[s] before arriving on afull[a], so
-        // afull also orders the TMA-written activation tile before the MMA.
         const uint32_t idesc = ptx::idesc_i8(kTileN, p.BN);
         const uint64_t desc0 = ptx::sw128_kmajor_desc(smem_base);
         const uint32_t stage_desc = p.stage_bytes >> 4;
         const uint32_t atom_desc = (p.BN * kXAtom) >> 4;
         uint32_t kb = static_cast<uint32_t>(beg % KB);
-        uint32_t s = 0, a = 0, aph = 0, as = 0, acc_ph = 0;
+        uint32_t s = 0, ph = 0, a = 0, aph = 0, as = 0, acc_ph = 0;
         for (uint32_t i = 0; i < n_local; ++i) {
             const bool seg_start = (i == 0) || (kb == 0);
             const bool seg_end = (kb == KB - 1) || (i + 1 == n_local);
             if (seg_start) ptx::mbar_wait(accempty_bar(as), acc_ph ^ 1);
             ptx::mbar_wait(afull_bar(a), aph);
+            ptx::mbar_wait(xfull_bar(s), ph);
+            if (i == 0 && lane == 0) LQG_T(4);
+            if (i + 1 == n_local && lane == 0) LQG_T(5);
             ptx::tc_fence_after();
             if (ptx::elect_one()) {
                 const uint32_t d_tmem = tmem_base + as * tp.acc_stride;
@@ -267,7 +349,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 acc_ph ^= 1;
             }
             if (++kb == KB) kb = 0;
-            if (++s == S) s = 0;
+            if (++s == S) {
+                s = 0;
+                ph ^= 1;
+            }
             if (++a == tp.a_slots) {
                 a = 0;
                 aph ^= 1;
@@ -288,7 +373,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint8_t* ring_w = smem + x_bytes;
         const uint32_t a_base = tmem_base + lane_addr + tp.a_base + wg * kHalf * 8;
         for (uint32_t i = 0; i < n_local; ++i) {
-            ptx::mbar_wait(full_bar(s), ph);
+            ptx::mbar_wait(wfull_bar(s), ph);
+            if (i == 0 && warp == 4 && lane == 0) LQG_T(3);
             ptx::mbar_wait(aempty_bar(a), aph ^ 1);
             ptx::tc_fence_after();
             const uint8_t* wchunk = ring_w + s * p.stage_bytes;
@@ -307,10 +393,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t sc = sa[cc] & 0xFFu;
                 const uint32_t a4 = (sa[cc] >> 8) * 0x01010101u;
                 uint32_t o[8];
+#ifdef LQG_EXP_NODEQUANT
+                o[0] = v[cc].x; o[1] = v[cc].y; o[2] = v[cc].z; o[3] = v[cc].w;
+                o[4] = sc; o[5] = a4; o[6] = v[cc].x; o[7] = v[cc].y;
+#else
                 lqq_dequant_word(v[cc].x, sc, a4, o[0], o[1]);
                 lqq_dequant_word(v[cc].y, sc, a4, o[2], o[3]);
                 lqq_dequant_word(v[cc].z, sc, a4, o[4], o[5]);
                 lqq_dequant_word(v[cc].w, sc, a4, o[6], o[7]);
+#endif
                 ptx::tmem_st_x8(a_taddr + cc * 8, o);
             }
             ptx::tmem_st_wait();
@@ -333,6 +424,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t lane_addr = (sp * 32) << 16;
         const uint32_t et = threadIdx.x - 12 * 32;  // 0..127
         const uint32_t nchunks = p.BN / 16;
+        const bool scaled = p.out_kind != kOutAcc;
+        ptx::griddep_wait();
         uint32_t as = 0, acc_ph = 0;
         uint32_t i = 0;
         while (i < n_local) {
@@ -345,8 +438,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t nt = static_cast<uint32_t>(tile - uint64_t(mt) * p.NT);
             const uint32_t n = nt * kTileN + row;
             const uint32_t m0 = mt * p.BN;
-            const double cs = p.out_kind == kOutAcc ? 0.0 : double(p.cs[n]);
+            // Scales are fetched while the MMAs of this segment are in flight:
+            // the token scales of the tile go to shared memory (read back as
+            // broadcasts), the channel scale of this thread's row to a register.
+            const double cs = scaled ? double(p.cs[n]) : 0.0;
+            if (scaled)
+                for (uint32_t j = et; j < p.BN; j += 128)
+                    ts_s[j] = m0 + j < p.M ? p.ts[m0 + j] : 0.f;
+            asm volatile("bar.sync 1, 128;" ::: "memory");
             ptx::mbar_wait(accfull_bar(as), acc_ph);
+            if (i >= n_local && et == 0) LQG_T(6);
             ptx::tc_fence_after();
             const uint32_t acc_taddr = tmem_base + lane_addr + as * tp.acc_stride;
             const uint32_t cur_as = as;
@@ -369,14 +470,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                         for (uint32_t j = 0; j < 16; ++j) {
                             const uint32_t m = m0 + ch * 16 + j;
-                            if (m < p.M)
-                                store_out(p, m, n, int32_t(v[j]), cs,
-                                          p.out_kind == kOutAcc ? 0.f : p.ts[m]);
+                            if (m < p.M) store_out(p, m, n, int32_t(v[j]), cs, ts_s[ch * 16 + j]);
                         }
                     }
                 }
             } else {
-                // split tile: exact INT32 reduction through the workspace
+                // split tile: exact INT32 reduction through the workspace. Every
+                // contributor adds its partial with red.add, the epilogue warps
+                // meet at a named barrier, and one acq_rel atomic on the tile
+                // counter both publishes those adds and elects the last arriver,
+                // which reads the sum back, applies the epilogue and re-zeroes.
                 const uint32_t slot = split_slot(tile, KB, G, p.total_iters);
                 int32_t* wsl = p.ws + uint64_t(slot) * (kMaxBN * kTileN);
                 for (uint32_t ch = 0; ch < nchunks; ++ch) {
@@ -390,18 +493,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
 #pragma unroll
                     for (uint32_t j = 0; j < 16; ++j)
-                        atomicAdd(wsl + (ch * 16 + j) * kTileN + row, int32_t(v[j]));
+                        ptx::red_add_s32(wsl + (ch * 16 + j) * kTileN + row, int32_t(v[j]));
                 }
-                __threadfence();
                 asm volatile("bar.sync 1, 128;" ::: "memory");
                 if (et == 0) {
-                    const uint32_t old = atomicAdd(p.counters + slot, n_iters);
+                    const uint32_t old = ptx::atom_add_acq_rel_gpu(p.counters + slot, n_iters);
                     *epi_flag = (old + n_iters == KB) ? 1u : 0u;
                 }
                 asm volatile("bar.sync 1, 128;" ::: "memory");
                 const bool last = *epi_flag != 0;
                 if (last) {
-                    __threadfence();
                     for (uint32_t ch = 0; ch < nchunks; ++ch) {
                         int32_t* cell = wsl + ch * 16 * kTileN + row;
                         int32_t v[16];
@@ -413,23 +514,23 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                             for (uint32_t j = 0; j < 16; ++j) {
                                 const uint32_t m = m0 + ch * 16 + j;
-                                if (m < p.M)
-                                    store_out(p, m, n, v[j], cs,
-                                              p.out_kind == kOutAcc ? 0.f : p.ts[m]);
+                                if (m < p.M) store_out(p, m, n, v[j], cs, ts_s[ch * 16 + j]);
                             }
                         }
                     }
                     if (et == 0) p.counters[slot] = 0;
                 }
-                asm volatile("bar.sync 1, 128;" ::: "memory");
             }
+            asm volatile("bar.sync 1, 128;" ::: "memory");  // ts_s / epi_flag reuse
         }
     }
 
+    if (warp == 12 && lane == 0) LQG_T(7);
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
-    if (warp == 2) ptx::tmem_dealloc(tmem_base, kTmemCols);
+    if (threadIdx.x == 0) LQG_T(8);
+    if (warp == 2) ptx::tmem_dealloc(tmem_base, p.tmem_cols);
 }
 
 }  // namespace lqg
