@@ -252,10 +252,11 @@ def run_lqg(args, workload):
     gen = torch.Generator(device=dev)
 
     # ---- weights: N-split shards, quantized on the GPU (LiquidQuant two-level)
+    from paper_2509_01229_b200 import tp
     layers = []
     for li, (name, n, k) in enumerate(shapes):
-        assert n % world == 0
-        nr = n // world
+        plan = tp.ShardPlan(n, world, rank, tp.shard_rows(n, world))
+        nr = plan.rows[1] - plan.rows[0]
         gen.manual_seed(1234 + 7919 * li + 104729 * rank)
         w = torch.randn(nr, k, generator=gen, device=dev, dtype=torch.float32).mul_(0.02)
         mask = torch.rand(nr, k, generator=gen, device=dev) < 1e-3
@@ -263,7 +264,7 @@ def run_lqg(args, workload):
         del mask
         dw = lqg.DeviceWeights.quantize(w, GROUP)
         del w
-        layers.append(dict(name=name, n=n, nr=nr, k=k, dw=dw))
+        layers.append(dict(name=name, n=n, nr=nr, k=k, dw=dw, plan=plan))
     torch.cuda.synchronize()
 
     # ---- activations per K, quantized per token on the GPU
@@ -278,8 +279,6 @@ def run_lqg(args, workload):
         del x
     ys = {L["name"]: torch.empty(mmax, L["nr"], dtype=torch.bfloat16, device=dev) for L in layers}
     if world > 1:
-        gath = {L["name"]: torch.empty(world * mmax * L["nr"], dtype=torch.bfloat16, device=dev)
-                for L in layers}
         yfull = {L["name"]: torch.empty(mmax, L["n"], dtype=torch.bfloat16, device=dev)
                  for L in layers}
     ws = lqg.Workspace(local)
@@ -288,10 +287,7 @@ def run_lqg(args, workload):
         q, ts = xs[L["k"]]
         L["dw"].gemm(q[:m], ts[:m], out=ys[L["name"]][:m], workspace=ws)
         if world > 1:
-            nr = L["nr"]
-            g = gath[L["name"]][: world * m * nr]
-            dist.all_gather_into_tensor(g, ys[L["name"]][:m])
-            yfull[L["name"]][:m].view(m, world, nr).copy_(g.view(world, m, nr).transpose(0, 1))
+            tp.gather_columns(ys[L["name"]][:m], L["plan"], out=yfull[L["name"]][:m])
 
     def step():
         for m in msweep:
@@ -463,6 +459,8 @@ def run_e2e(args, layers, msweep, xs, world, dev, lqg, ops_step):
     shard, NCCL all-gather, D2H of the full Y."""
     import torch
     import torch.distributed as dist
+
+    from paper_2509_01229_b200 import tp
     mmax = max(msweep)
     hx = {k: (q.cpu().pin_memory(), ts.cpu().pin_memory()) for k, (q, ts) in xs.items()}
     hy = {L["name"]: torch.empty(mmax, L["n"], dtype=torch.bfloat16).pin_memory() for L in layers}
@@ -471,7 +469,7 @@ def run_e2e(args, layers, msweep, xs, world, dev, lqg, ops_step):
     if world > 1:
         dx = {k: (torch.empty_like(q, device=dev), torch.empty_like(ts, device=dev)) for k, (q, ts) in xs.items()}
         dy = {L["name"]: torch.empty(mmax, L["nr"], dtype=torch.bfloat16, device=dev) for L in layers}
-        dg = {L["name"]: torch.empty(world * mmax * L["nr"], dtype=torch.bfloat16, device=dev) for L in layers}
+        yd = {L["name"]: torch.empty(mmax, L["n"], dtype=torch.bfloat16, device=dev) for L in layers}
 
     def one_step():
         for m in msweep:
@@ -484,10 +482,8 @@ def run_e2e(args, layers, msweep, xs, world, dev, lqg, ops_step):
                     qd[:m].copy_(qh[:m], non_blocking=True)
                     td[:m].copy_(th[:m], non_blocking=True)
                     L["dw"].gemm(qd[:m], td[:m], out=dy[L["name"]][:m])
-                    nr = L["nr"]
-                    g = dg[L["name"]][: world * m * nr]
-                    dist.all_gather_into_tensor(g, dy[L["name"]][:m])
-                    hy[L["name"]][:m].view(m, world, nr).copy_(g.view(world, m, nr).transpose(0, 1))
+                    tp.gather_columns(dy[L["name"]][:m], L["plan"], out=yd[L["name"]][:m])
+                    hy[L["name"]][:m].copy_(yd[L["name"]][:m])
                     torch.cuda.synchronize()
 
     one_step()

@@ -98,6 +98,21 @@ int lqg_bundle_validate(const lqg_bundle_view* bundle);
  * (gemm.cpp:151-165). */
 int lqg_weights_create(const lqg_bundle_view* bundle, int device, lqg_weights** out);
 
+/* Device image (prepacked layout) size in bytes for an
+ * n x k bundle with this group size; 0 if the device layout cannot hold it. */
+uint64_t lqg_image_bytes(uint32_t n, uint32_t k, uint32_t group_size);
+
+/* Host-only prepack (no GPU needed): validates like lqg_weights_create and
+ * writes the device image into `image` (lqg_image_bytes bytes). Lets callers
+ * prepack once offline and cache the result (see lqg_weights_from_image). */
+int lqg_prepack_host(const lqg_bundle_view* bundle, uint8_t* image, uint64_t image_bytes);
+
+/* Uploads a prepacked image (from lqg_prepack_host or a cache file) plus the n
+ * channel scales to `device`. */
+int lqg_weights_from_image(const uint8_t* image, uint64_t image_bytes, const float* channel_scales,
+                           uint32_t n, uint32_t k, uint32_t group_size, int device,
+                           lqg_weights** out);
+
 /* Quantizes device FP32 weights w[n][k] (row pitch ldw floats) on the GPU with
  * the reference's two-level LiquidQuant quantizer (build_bundle,
  * quant.cpp:203-232; bit-exact) straight into the device layout. */

@@ -75,6 +75,8 @@ def lib() -> C.CDLL:
     sig = {
         "lqg_bundle_validate": [C.POINTER(BundleViewC)],
         "lqg_weights_create": [C.POINTER(BundleViewC), i32, C.POINTER(vp)],
+        "lqg_prepack_host": [C.POINTER(BundleViewC), vp, C.c_uint64],
+        "lqg_weights_from_image": [vp, C.c_uint64, vp, u32, u32, u32, i32, C.POINTER(vp)],
         "lqg_weights_quantize": [vp, i64, u32, u32, u32, vp, C.POINTER(vp)],
         "lqg_weights_destroy": [vp],
         "lqg_weights_shape": [vp, C.POINTER(u32), C.POINTER(u32), C.POINTER(u32)],
@@ -92,6 +94,8 @@ def lib() -> C.CDLL:
         f = getattr(L, name)
         f.argtypes = args
         f.restype = C.c_int
+    L.lqg_image_bytes.argtypes = [u32, u32, u32]
+    L.lqg_image_bytes.restype = C.c_uint64
     L.lqg_weights_device_bytes.argtypes = [vp]
     L.lqg_weights_device_bytes.restype = C.c_uint64
     L.lqg_kernel_launch_count.restype = C.c_uint64
@@ -103,7 +107,8 @@ def lib() -> C.CDLL:
 
 # Symbols declared in include/lqg.h (checked by tests/test_boundary.py).
 EXPORTS = [
-    "lqg_bundle_validate", "lqg_weights_create", "lqg_weights_quantize", "lqg_weights_destroy",
+    "lqg_bundle_validate", "lqg_image_bytes", "lqg_prepack_host", "lqg_weights_from_image",
+    "lqg_weights_create", "lqg_weights_quantize", "lqg_weights_destroy",
     "lqg_weights_shape", "lqg_weights_export", "lqg_weights_device_bytes",
     "lqg_workspace_create", "lqg_workspace_destroy", "lqg_gemm_w4a8", "lqg_gemm_w4a8_accum",
     "lqg_gemm_w4a8_host", "lqg_gemm_w4a8_accum_host", "lqg_dequant_weights",

@@ -466,6 +466,57 @@ int lqg_bundle_validate(const lqg_bundle_view* bundle) {
     return validate_bundle(*bundle);
 }
 
+uint64_t lqg_image_bytes(uint32_t n, uint32_t k, uint32_t group_size) {
+    if (n < 1 || k < 1 || group_size < 1 || group_size % 32 != 0) return 0;
+    const ImageGeom G = make_geom(n, k, group_size);
+    return uint64_t(G.NT) * G.KB * G.chunk_bytes;
+}
+
+int lqg_prepack_host(const lqg_bundle_view* bundle, uint8_t* image, uint64_t image_bytes) {
+    if (!bundle || !image) return set_err(LQG_EVALIDATION, "null argument");
+    int rc = validate_bundle(*bundle);
+    if (rc) return rc;
+    rc = device_layout_supported(bundle->group_size);
+    if (rc) return rc;
+    const ImageGeom G = make_geom(bundle->n, bundle->k, bundle->group_size);
+    if (image_bytes != uint64_t(G.NT) * G.KB * G.chunk_bytes)
+        return set_err(LQG_EVALIDATION, "image buffer has wrong size");
+    std::vector<uint8_t> img;
+    prepack_host(*bundle, G, img);
+    std::memcpy(image, img.data(), img.size());
+    return LQG_OK;
+}
+
+int lqg_weights_from_image(const uint8_t* image, uint64_t image_bytes, const float* channel_scales,
+                           uint32_t n, uint32_t k, uint32_t group_size, int device,
+                           lqg_weights** out) {
+    if (!image || !channel_scales || !out) return set_err(LQG_EVALIDATION, "null argument");
+    if (n < 1 || k < 1 || group_size < 1 || k % group_size != 0)
+        return set_err(LQG_EVALIDATION, "bad image dimensions");
+    int rc = device_layout_supported(group_size);
+    if (rc) return rc;
+    const ImageGeom G = make_geom(n, k, group_size);
+    if (image_bytes != uint64_t(G.NT) * G.KB * G.chunk_bytes)
+        return set_err(LQG_EVALIDATION, "image buffer has wrong size");
+    for (uint32_t r = 0; r < n; ++r)
+        if (!(channel_scales[r] > 0.0f) || !std::isfinite(channel_scales[r]))
+            return set_err(LQG_EVALIDATION, "channel scale at row " + std::to_string(r) +
+                                                " must be positive and finite");
+    lqg_weights* w = nullptr;
+    rc = alloc_weights(device, G, &w);
+    if (rc) return rc;
+    std::vector<float> cs(uint64_t(G.NT) * kTileN, 1.0f);
+    std::memcpy(cs.data(), channel_scales, uint64_t(n) * 4);
+    DeviceGuard g(device);
+    if (cudaMemcpy(w->d_img, image, image_bytes, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(w->d_cs, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
+        lqg_weights_destroy(w);
+        return set_err(LQG_ECUDA, "weight upload failed");
+    }
+    *out = w;
+    return LQG_OK;
+}
+
 int lqg_weights_create(const lqg_bundle_view* bundle, int device, lqg_weights** out) {
     if (!bundle || !out) return set_err(LQG_EVALIDATION, "null argument");
     int rc = validate_bundle(*bundle);
@@ -473,21 +524,10 @@ int lqg_weights_create(const lqg_bundle_view* bundle, int device, lqg_weights** 
     rc = device_layout_supported(bundle->group_size);
     if (rc) return rc;
     const ImageGeom G = make_geom(bundle->n, bundle->k, bundle->group_size);
-    lqg_weights* w = nullptr;
-    rc = alloc_weights(device, G, &w);
-    if (rc) return rc;
     std::vector<uint8_t> img;
     prepack_host(*bundle, G, img);
-    std::vector<float> cs(uint64_t(G.NT) * kTileN, 1.0f);
-    std::memcpy(cs.data(), bundle->channel_scales, bundle->n * 4);
-    DeviceGuard g(device);
-    if (cudaMemcpy(w->d_img, img.data(), img.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy(w->d_cs, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
-        lqg_weights_destroy(w);
-        return set_err(LQG_ECUDA, "weight upload failed");
-    }
-    *out = w;
-    return LQG_OK;
+    return lqg_weights_from_image(img.data(), img.size(), bundle->channel_scales, bundle->n,
+                                  bundle->k, bundle->group_size, device, out);
 }
 
 int lqg_weights_quantize(const float* d_w, int64_t ldw, uint32_t n, uint32_t k, uint32_t group_size,

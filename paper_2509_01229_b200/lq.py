@@ -143,6 +143,20 @@ class QuantizedWeightBundle:
         v, _keep = self._view()
         check(_lib.lib().lqg_bundle_validate(C.byref(v)))
 
+    def prepack(self) -> np.ndarray:
+        """The device image of this bundle (host-only, no GPU needed); cache it
+        and upload later with DeviceWeights.from_image."""
+        if self.group_scales.size != self.group_offsets.size:
+            raise ValidationError("group parameter arrays have wrong size")
+        nbytes = int(_lib.lib().lqg_image_bytes(self.n, self.k, self.group_size))
+        if nbytes == 0:
+            raise ValidationError("the sm_100a device layout needs group_size % 32 == 0 (got "
+                                  f"{self.group_size})")
+        img = np.empty(nbytes, np.uint8)
+        v, _keep = self._view()
+        check(_lib.lib().lqg_prepack_host(C.byref(v), img.ctypes.data, nbytes))
+        return img
+
     def device_weights(self, device: int = 0) -> "DeviceWeights":
         """The prepacked device copy (created on first use, then cached)."""
         dw = self._device.get(device)
@@ -298,6 +312,19 @@ class DeviceWeights:
         v, _keep = b._view()
         h = C.c_void_p()
         check(_lib.lib().lqg_weights_create(C.byref(v), device, C.byref(h)))
+        return cls(h, device)
+
+    @classmethod
+    def from_image(cls, image: np.ndarray, channel_scales: np.ndarray, n: int, k: int,
+                   group_size: int, device: int = 0) -> "DeviceWeights":
+        """Upload a prepacked image (QuantizedWeightBundle.prepack / a cache file)."""
+        img = np.ascontiguousarray(image, np.uint8)
+        cs = np.ascontiguousarray(channel_scales, np.float32)
+        if cs.size != n:
+            raise ValidationError("channel scale array has wrong size")
+        h = C.c_void_p()
+        check(_lib.lib().lqg_weights_from_image(img.ctypes.data, img.size, cs.ctypes.data, n, k,
+                                                group_size, device, C.byref(h)))
         return cls(h, device)
 
     @classmethod
