@@ -323,3 +323,18 @@ def test_launch_counter_counts_native_kernels(torch_cuda, lqg):
     dw.gemm(q, ts)
     dw.gemm_accum(q)
     assert lqg.launch_count() - c0 == 2
+
+
+def test_reference_acceptance_gate_through_cpp_dropin(torch_cuda):
+    """The reference's own acceptance criterion 6 (acceptance.cpp:265-315: 100
+    random GEMMs, both engines, both layouts, three tile configs, bit-exact vs
+    the int64 oracle, F32 within 1e-6) with lq::gemm_w4a8[_accum] provided by
+    integration/lq_gemm_lqg.cpp over the lqg C ABI (built by oracle/Makefile
+    `dropin` from the reference sources into oracle/_ref/)."""
+    import subprocess
+    binary = os.path.join(os.path.dirname(GOLD), "..", "oracle", "_ref", "acceptance_lqg")
+    if not os.path.exists(binary):
+        pytest.skip("oracle/_ref/acceptance_lqg not built (reference sources absent)")
+    r = subprocess.run([binary, "--criterion", "6"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "[PASS] criterion 6" in r.stdout, r.stdout
