@@ -12,7 +12,7 @@ import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-LIB_PATH = os.path.join(HERE, "liblqg.so")
+LIB_PATH = os.environ.get("LQG_LIB_PATH") or os.path.join(HERE, "liblqg.so")
 CSRC = os.path.join(HERE, "csrc")
 SOURCES = ["lqg_api.cu"]
 HEADERS = ["lqg_gemm.cuh", "lqg_aux.cuh", "lqg_layout.h", "sm100_ptx.cuh"]
@@ -32,16 +32,18 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile liblqg.so for sm_100a (cross-compiles without a GPU)."""
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, defines: tuple = (), out: str | None = None) -> str:
+    """Compile liblqg.so for sm_100a (cross-compiles without a GPU). `defines`
+    and `out` build debug variants (e.g. -DLQG_TRACE into liblqg_trace.so)."""
+    target = out or LIB_PATH
+    if not force and not out and not _stale():
         return LIB_PATH
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, *(["-Xptxas", "-v"] if verbose else []),
-           "-o", LIB_PATH + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES]]
+    cmd = [nvcc, *NVCC_FLAGS, *(["-Xptxas", "-v"] if verbose else []), *[f"-D{d}" for d in defines],
+           "-o", target + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES]]
     subprocess.run(cmd, check=True)
-    os.replace(LIB_PATH + ".tmp", LIB_PATH)
-    return LIB_PATH
+    os.replace(target + ".tmp", target)
+    return target
 
 
 class FragmentDescriptorC(C.Structure):
@@ -66,7 +68,8 @@ def lib() -> C.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    if _stale() and os.path.exists(os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")):
+    if (not os.environ.get("LQG_LIB_PATH") and _stale()
+            and os.path.exists(os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc"))):
         build()
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback)")

@@ -92,14 +92,13 @@ EncodeTiledFn encode_fn() {
 
 // ---------------------------------------------------------------- workspace
 constexpr uint32_t kMaxSlots = 160;  // >= SM count of any sm_100 part
-constexpr uint64_t kSlotInts = 256ull * kTileN;
+constexpr uint64_t kSlotCells = 256ull * kTileN;  // INT32 partial-sum cells per CTA
 
 }  // namespace
 
 struct lqg_workspace {
     int device = 0;
-    int32_t* ws = nullptr;
-    uint32_t* counters = nullptr;
+    int32_t* parts = nullptr;  // [kMaxSlots][kSlotCells], INT32_MIN = not published
 };
 
 struct lqg_weights {
@@ -125,14 +124,11 @@ int workspace_create(int dev, lqg_workspace** out) {
     auto* w = new lqg_workspace();
     w->device = dev;
     DeviceGuard g(dev);
-    if (cudaMalloc(&w->ws, kMaxSlots * kSlotInts * 4) != cudaSuccess ||
-        cudaMalloc(&w->counters, kMaxSlots * 4) != cudaSuccess) {
-        cudaFree(w->ws);
+    if (cudaMalloc(&w->parts, kMaxSlots * kSlotCells * 4) != cudaSuccess) {
         delete w;
         return set_err(LQG_ECUDA, "workspace allocation failed");
     }
-    cudaMemset(w->ws, 0, kMaxSlots * kSlotInts * 4);
-    cudaMemset(w->counters, 0, kMaxSlots * 4);
+    fill_i32_kernel<<<592, 256>>>(w->parts, kMaxSlots * kSlotCells, INT32_MIN);
     if (cudaDeviceSynchronize() != cudaSuccess) return set_err(LQG_ECUDA, "workspace memset failed");
     *out = w;
     return LQG_OK;
@@ -311,7 +307,7 @@ int alloc_weights(int dev, const ImageGeom& G, lqg_weights** out) {
 // TMEM (2 x 192 columns + a 2-slot A ring, see tmem_plan).
 constexpr uint32_t kMaxTileM = 192;
 // Token tiles up to this size run in decode mode (see launch_gemm).
-constexpr uint32_t kDecodeMaxBN = 64;
+constexpr uint32_t kDecodeMaxBN = 32;
 
 uint32_t env_u32(const char* name, uint32_t dflt) {
     const char* v = std::getenv(name);
@@ -367,8 +363,7 @@ int launch_gemm(const lqg_weights* w, const int8_t* d_x, int64_t ldx, const floa
     p.ts = d_ts;
     p.out = d_out;
     p.ldo = ldo;
-    p.ws = W->ws;
-    p.counters = W->counters;
+    p.parts = W->parts;
     p.M = m;
     p.N = G.n;
     p.KB = G.KB;
@@ -379,13 +374,20 @@ int launch_gemm(const lqg_weights* w, const int8_t* d_x, int64_t ldx, const floa
     p.chunk_bytes = G.chunk_bytes;
     p.out_kind = out_kind;
     p.stage_bytes = (BN * kKBlock + G.chunk_bytes + 1023) / 1024 * 1024;
-    // Decode mode (small token tiles): <= 110 KB of shared memory and 256 TMEM
-    // columns, so two CTAs fit on an SM and the next GEMM in the stream (PDL)
-    // can stream its weights while this one drains. Otherwise one CTA per SM.
-    const bool decode = BN <= kDecodeMaxBN && !env_u32("LQG_DEBUG_NO_DECODE_MODE", 0);
+    // Co-resident mode (opt-in, LQG_CORESIDENT=1, small token tiles only): <= 110
+    // KB of shared memory and 256 TMEM columns so that two CTAs fit on an SM
+    // and the next GEMM's CTAs are resident while this one drains. Measured on
+    // B200 it loses to one CTA per SM with the full 227 KB ring (LLaMA-2-70B
+    // 4-layer step at M = 16: 93.9 vs 83.5 us): the halved ring and the
+    // 72-register cap slow the mainloop more than the earlier start gains.
+    const bool decode = BN <= kDecodeMaxBN && env_u32("LQG_CORESIDENT", 0);
     p.tmem_cols = decode ? 256 : 512;
     // ~24 MB of weights across the grid (enough to cover a kernel tail at HBM rate).
-    p.l2_prefetch = env_u32("LQG_L2_PREFETCH_CHUNKS", decode ? 10 : 0);
+    p.l2_prefetch = env_u32("LQG_L2_PREFETCH_CHUNKS", decode ? 4 : 0);
+    p.w_split = std::max(1u, env_u32("LQG_DEBUG_WSPLIT", 1));
+    p.pdl_trigger = env_u32("LQG_PDL_TRIGGER", decode ? 2 : 0);
+    p.prewait_stages = env_u32("LQG_PREWAIT_STAGES", kMaxStages);
+    p.trace_slot = static_cast<uint32_t>(g_launches.load(std::memory_order_relaxed) % 8);
     const uint32_t budget = decode ? 110 * 1024 - 3072 : 227 * 1024 - 3072;
     p.stages = std::min<uint32_t>(kMaxStages, budget / p.stage_bytes);
     if (uint32_t st = env_u32("LQG_DEBUG_STAGES", 0)) p.stages = std::min(p.stages, st);
@@ -393,17 +395,38 @@ int launch_gemm(const lqg_weights* w, const int8_t* d_x, int64_t ldx, const floa
     if (tmem_plan(BN, p.tmem_cols).a_slots < 1)
         return set_err(LQG_EVALIDATION, "tile configuration does not fit tensor memory");
     p.total_iters = uint64_t(MT) * G.NT * G.KB;
+    if (p.total_iters * kMaxSlots >= (uint64_t(1) << 32))
+        return set_err(LQG_EVALIDATION, "problem too large for one launch (tiles x k-blocks x " +
+                                            std::to_string(kMaxSlots) + " >= 2^32)");
     uint32_t grid = static_cast<uint32_t>(
         std::min<uint64_t>(std::min<uint32_t>(w->num_sms, kMaxSlots), p.total_iters));
     if (uint32_t gd = env_u32("LQG_DEBUG_GRID", 0))
         grid = static_cast<uint32_t>(std::min<uint64_t>({gd, uint64_t(kMaxSlots), p.total_iters}));
+    // Hybrid schedule: whole-tile rounds first, stream-K over the last G..2G
+    // tiles (all tiles when there are fewer than G), tiles rasterized in groups
+    // of GM token tiles sized so that the activation and weight slices of one
+    // round balance in L2 (GM^2 ~ G * weight bytes per tile / activation bytes).
+    {
+        const uint64_t T = uint64_t(MT) * G.NT;
+        uint32_t dp = 0;
+        if (!decode && T >= grid && !env_u32("LQG_DEBUG_NO_DP", 0))
+            dp = static_cast<uint32_t>(T % grid == 0 ? T / grid : T / grid - 1);
+        p.dp_rounds = dp;
+        const double ratio = double(grid) * (kTileN / 2.0) / double(BN);
+        uint32_t gm = static_cast<uint32_t>(std::lround(std::sqrt(ratio)));
+        if (uint32_t e = env_u32("LQG_DEBUG_RASTER_GM", 0)) gm = e;
+        p.raster_gm = std::max(1u, std::min(gm, MT));
+    }
     const size_t smem = size_t(p.stages) * p.stage_bytes + 1024 + 2048;
 
     DeviceGuard dg(w->device);
     cudaError_t e = cudaSuccess;
     std::call_once(g_attr_once[w->device % 64], [&] {
-        e = cudaFuncSetAttribute(lqg_w4a8_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 227 * 1024);
+        e = cudaFuncSetAttribute(lqg_w4a8_gemm_kernel<true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(lqg_w4a8_gemm_kernel<false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     });
     if (e != cudaSuccess) return set_err(LQG_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
     cudaLaunchConfig_t cfg{};
@@ -416,7 +439,10 @@ int launch_gemm(const lqg_weights* w, const int8_t* d_x, int64_t ldx, const floa
     attr[0].val.programmaticStreamSerializationAllowed = env_u32("LQG_DEBUG_NO_PDL", 0) ? 0 : 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel, tmap, p));
+    if (decode)
+        LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<true>, tmap, p));
+    else
+        LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<false>, tmap, p));
     g_launches.fetch_add(1, std::memory_order_relaxed);
     LQG_CUDA(cudaGetLastError());
     return LQG_OK;
@@ -452,7 +478,7 @@ const char* lqg_last_error(void) { return g_err.c_str(); }
 #ifdef LQG_TRACE
 // Debug build only: copy the per-CTA %globaltimer trace (160 x 16 u64).
 int lqg_debug_trace(unsigned long long* out) {
-    return cudaMemcpyFromSymbol(out, g_lqg_trace, sizeof(unsigned long long) * 160 * 16) ==
+    return cudaMemcpyFromSymbol(out, g_lqg_trace, sizeof(unsigned long long) * 8 * 160 * 16) ==
                    cudaSuccess
                ? 0
                : 4;
@@ -661,8 +687,7 @@ int lqg_workspace_create(int device, lqg_workspace** out) {
 int lqg_workspace_destroy(lqg_workspace* ws) {
     if (!ws) return LQG_OK;
     DeviceGuard g(ws->device);
-    cudaFree(ws->ws);
-    cudaFree(ws->counters);
+    cudaFree(ws->parts);
     delete ws;
     return LQG_OK;
 }

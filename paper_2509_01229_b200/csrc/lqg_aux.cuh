@@ -19,6 +19,12 @@ __device__ __forceinline__ int round_half_away(double v) {
     return static_cast<int>(v < 0 ? v - 0.5 : v + 0.5);
 }
 
+__global__ void fill_i32_kernel(int32_t* p, uint64_t n, int32_t v) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        p[i] = v;
+}
+
 __global__ void fill_image_kernel(uint8_t* img, uint64_t nchunks, uint32_t chunk_bytes) {
     const uint64_t words_per_chunk = chunk_bytes / 4;
     const uint64_t total = nchunks * words_per_chunk;

@@ -63,17 +63,16 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         : "memory");
 }
 
-// ---------------------------------------------------------------- global atomics
-__device__ __forceinline__ void red_add_s32(int32_t* addr, int32_t v) {
-    asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(addr), "r"(v) : "memory");
-}
-// Acquire-release fetch-add at GPU scope: publishes the calling CTA's prior
-// writes (ordered before it by a CTA barrier) and acquires the others'.
-__device__ __forceinline__ uint32_t atom_add_acq_rel_gpu(uint32_t* addr, uint32_t v) {
-    uint32_t old;
-    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(addr), "r"(v)
+// ---------------------------------------------------------------- global memory
+// Re-read of four 32-bit words at GPU scope (each element single-copy atomic,
+// not served from L1): used to spin on split-K cells.
+__device__ __forceinline__ int4 ld_relaxed_v4(const int4* addr) {
+    int4 v;
+    asm volatile("ld.relaxed.gpu.global.v4.s32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(addr)
                  : "memory");
-    return old;
+    return v;
 }
 
 // ---------------------------------------------------------------- L2 policies

@@ -1,0 +1,67 @@
+"""A/B timing of liblqg variants in one process per variant, alternated:
+  python tools/ab.py --libs a.so,b.so --ms 16 --rounds 3
+Times the 70B 4-layer step at each M as a CUDA graph (3 rotations), like bench.py."""
+import argparse, json, os, subprocess, sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CHILD = r'''
+import os, sys, json
+sys.path.insert(0, ROOT)
+import torch
+import paper_2509_01229_b200 as lqg
+shapes = [(10240, 8192), (8192, 8192), (28672, 8192), (8192, 28672)]
+ms = MS
+g = torch.Generator(device="cuda"); g.manual_seed(1)
+layers = [lqg.DeviceWeights.quantize(torch.randn(n, k, generator=g, device="cuda") * 0.02, 128) for n, k in shapes]
+xs = {k: lqg.quantize_activations(torch.randn(max(ms), k, generator=g, device="cuda")) for k in (8192, 28672)}
+ys = [torch.empty(max(ms), n, dtype=torch.bfloat16, device="cuda") for n, _ in shapes]
+ws = lqg.Workspace(0)
+out = {}
+for m in ms:
+    def step():
+        for (n, k), dw, y in zip(shapes, layers, ys):
+            q, ts = xs[k]
+            dw.gemm(q[:m], ts[:m], out=y[:m], workspace=ws)
+    step(); torch.cuda.synchronize()
+    gr = torch.cuda.CUDAGraph(); s = torch.cuda.Stream(); s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s), torch.cuda.graph(gr, stream=s):
+        for _ in range(3): step()
+    torch.cuda.current_stream().wait_stream(s)
+    gr.replay(); torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    e0.record()
+    for _ in range(5): gr.replay()
+    e1.record(); torch.cuda.synchronize()
+    out[m] = e0.elapsed_time(e1) / 15 * 1e3
+print(json.dumps(out))
+'''
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--libs", required=True)
+    ap.add_argument("--ms", default="16")
+    ap.add_argument("--rounds", type=int, default=3)
+    ap.add_argument("--env", default="", help="extra env per lib, ';'-separated list of k=v,k=v")
+    a = ap.parse_args()
+    libs = a.libs.split(",")
+    envs = a.env.split(";") if a.env else [""] * len(libs)
+    ms = [int(x) for x in a.ms.split(",")]
+    res = {i: [] for i in range(len(libs))}
+    for r in range(a.rounds):
+        for i, lib in enumerate(libs):
+            env = dict(os.environ, LQG_LIB_PATH=os.path.abspath(lib))
+            for kv in filter(None, envs[i].split(",")):
+                k, v = kv.split("=")
+                env[k] = v
+            code = CHILD.replace("ROOT", repr(ROOT)).replace("MS", repr(ms))
+            o = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
+            if o.returncode:
+                print(lib, "FAILED", o.stderr[-500:]); continue
+            res[i].append(json.loads(o.stdout.strip().splitlines()[-1]))
+    for i, lib in enumerate(libs):
+        for m in ms:
+            v = [x[str(m)] for x in res[i]]
+            print(f"{os.path.basename(lib):28s} {envs[i]:30s} M={m:5d}: " + " ".join(f"{t:7.1f}" for t in v) + f"  min {min(v):.1f} us")
+
+if __name__ == "__main__":
+    main()
