@@ -223,22 +223,40 @@ __device__ __forceinline__ void tile_coords_p(uint32_t t, const GemmParams& p, u
 }
 
 // y = float(double(acc) * double(cs) * double(ts)) (quant.cpp:125-127), left
-// to right, then the requested cast (RNE). cs_d is double(cs).
-__device__ __forceinline__ void store_out(const GemmParams& p, uint32_t m, uint32_t n,
-                                          int32_t acc, double cs_d, float ts) {
-    const uint64_t idx = uint64_t(m) * uint64_t(p.ldo) + n;
-    if (p.out_kind == kOutAcc) {
-        static_cast<int32_t*>(p.out)[idx] = acc;
-        return;
+// to right, then the requested cast (RNE). cs_d is double(cs). One call stores
+// the 16 tokens [m0, m0+16) of output column n; the output kind is a template
+// parameter so every store loop is branch-free (dispatch once per chunk).
+template <uint32_t kKind>
+__device__ __forceinline__ void store_chunk_k(const GemmParams& p, uint32_t m0, uint32_t n,
+                                              const int32_t (&acc)[16], double cs_d,
+                                              const float* ts) {
+    const uint32_t mend = min(16u, p.M > m0 ? p.M - m0 : 0u);
+    uint64_t idx = uint64_t(m0) * uint64_t(p.ldo) + n;
+#pragma unroll
+    for (uint32_t j = 0; j < 16; ++j, idx += p.ldo) {
+        if (j >= mend) break;
+        if (kKind == kOutAcc) {
+            static_cast<int32_t*>(p.out)[idx] = acc[j];
+        } else {
+            const float y = __double2float_rn(__dmul_rn(__dmul_rn(double(acc[j]), cs_d), double(ts[j])));
+            if (kKind == kOutF32)
+                static_cast<float*>(p.out)[idx] = y;
+            else if (kKind == kOutF16)
+                static_cast<__half*>(p.out)[idx] = __float2half_rn(y);
+            else
+                static_cast<__nv_bfloat16*>(p.out)[idx] = __float2bfloat16_rn(y);
+        }
     }
-    const double yd = __dmul_rn(__dmul_rn(double(acc), cs_d), double(ts));
-    const float y = __double2float_rn(yd);
-    if (p.out_kind == kOutF32)
-        static_cast<float*>(p.out)[idx] = y;
-    else if (p.out_kind == kOutF16)
-        static_cast<__half*>(p.out)[idx] = __float2half_rn(y);
-    else
-        static_cast<__nv_bfloat16*>(p.out)[idx] = __float2bfloat16_rn(y);
+}
+
+__device__ __forceinline__ void store_chunk(const GemmParams& p, uint32_t m0, uint32_t n,
+                                            const int32_t (&acc)[16], double cs_d, const float* ts) {
+    switch (p.out_kind) {
+        case kOutAcc: store_chunk_k<kOutAcc>(p, m0, n, acc, cs_d, ts); break;
+        case kOutF32: store_chunk_k<kOutF32>(p, m0, n, acc, cs_d, ts); break;
+        case kOutF16: store_chunk_k<kOutF16>(p, m0, n, acc, cs_d, ts); break;
+        default: store_chunk_k<kOutBF16>(p, m0, n, acc, cs_d, ts); break;
+    }
 }
 
 #ifdef LQG_TRACE
@@ -371,7 +389,7 @@ __global__ void __launch_bounds__(kThreads, kDecode ? 2 : 1)
         auto x_next = [&]() {
             if (xw.next(p)) tile_coords_p(xw.tile, p, xmt, xnt);
         };
-        const uint32_t pre = min(min(n_local, S), p.prewait_stages);
+        const uint32_t pre = n_local < S ? n_local : S;
         for (uint32_t i = 0; i < pre; ++i) {
             if (ptx::elect_one()) {
                 ptx::mbar_arrive_expect_tx(wfull_bar(i), p.chunk_bytes);
@@ -609,11 +627,10 @@ __global__ void __launch_bounds__(kThreads, kDecode ? 2 : 1)
                         if (lane == 0) ptx::mbar_arrive(accempty_bar(cur_as));
                     }
                     if (n < p.N) {
+                        int32_t a[16];
 #pragma unroll
-                        for (uint32_t j = 0; j < 16; ++j) {
-                            const uint32_t m = m0 + ch * 16 + j;
-                            if (m < p.M) store_out(p, m, n, int32_t(v[j]), cs, ts_s[ch * 16 + j]);
-                        }
+                        for (uint32_t j = 0; j < 16; ++j) a[j] = int32_t(v[j]);
+                        store_chunk(p, m0 + ch * 16, n, a, cs, ts_s + ch * 16);
                     }
                 }
             } else if (kb0 > 0) {
@@ -729,13 +746,7 @@ __global__ void __launch_bounds__(kThreads, kDecode ? 2 : 1)
                         }
                     }
                     if (ch == 0 && et == 0) LQG_T(10);
-                    if (n < p.N) {
-#pragma unroll
-                        for (uint32_t j = 0; j < 16; ++j) {
-                            const uint32_t m = m0 + ch * 16 + j;
-                            if (m < p.M) store_out(p, m, n, sum[j], cs, ts_s[ch * 16 + j]);
-                        }
-                    }
+                    if (n < p.N) store_chunk(p, m0 + ch * 16, n, sum, cs, ts_s + ch * 16);
                 }
             }
             asm volatile("bar.sync 1, 128;" ::: "memory");  // ts_s reuse
