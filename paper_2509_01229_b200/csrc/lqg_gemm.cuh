@@ -103,6 +103,11 @@ struct GemmParams {
     uint32_t pdl_trigger;
     uint32_t prewait_stages;   // weight chunks requested before griddepcontrol.wait      // 0: after the prologue, 1: after the last load is issued, 2: after the last MMA
     uint64_t total_iters;      // MT*NT*KB
+    // dynamic (work-stealing) decode schedule, lqg_gemm_dyn.cuh
+    uint32_t unit_kb;          // k-blocks per work unit
+    uint32_t units_per_tile;   // ceil(KB / unit_kb)
+    uint32_t static_units;     // units [0, static_units) are assigned round-robin, the rest claimed
+    uint32_t* dcnt;            // claim counter, zero between launches
 };
 
 // LiquidQuant dequantization of one interleaved word (packed.cpp:63-71):
@@ -273,9 +278,6 @@ __device__ __forceinline__ void trace(uint32_t slot, uint32_t e) {
 #define LQG_TV(e, v) ((void)0)
 #endif
 
-#ifndef LQG_DECODE_NOPIPE
-#define LQG_DECODE_NOPIPE 0
-#endif
 // kDecode: two CTAs per SM (<= 110 KB SMEM, 256 TMEM columns, <= 72 registers)
 // so consecutive GEMMs overlap under PDL; otherwise one CTA per SM.
 template <bool kDecode>
@@ -588,22 +590,27 @@ __global__ void __launch_bounds__(kThreads, kDecode ? 2 : 1)
                 for (uint32_t j = et; j < p.BN; j += 128)
                     ts_s[j] = m0 + j < p.M ? p.ts[m0 + j] : 0.f;
             // Head piece of a split tile: find the contributors and start loading
-            // the first pair's chunk-0 cells now, while this segment's MMAs run.
+            // the first batch's chunk-0 cells now, while this segment's MMAs run.
             const bool finisher = n_iters < KB && kb0 == 0;
             uint32_t c_first = 0, c_end = 0;
-            int4 pre0[4], pre1[4];
+            // Split-K cells of up to four contributors for one 16-token chunk:
+            // [contributor][int4]. Loaded one chunk ahead (software pipeline).
+            int4 cb[4][4];
+            const int32_t* parts_row = p.parts + uint64_t(row) * 16;
+            auto load_batch = [&](uint32_t c, uint32_t ch) {
+                const uint32_t nb = min(4u, c_end - c);
+#pragma unroll
+                for (uint32_t b = 0; b < 4; ++b)
+                    if (b < nb) {
+                        const int4* cell = reinterpret_cast<const int4*>(
+                            parts_row + uint64_t(c + b) * (kMaxBN * kTileN) + uint64_t(ch) * kTileN * 16);
+#pragma unroll
+                        for (uint32_t q = 0; q < 4; ++q) cb[b][q] = __ldcg(cell + q);
+                    }
+            };
             if (finisher) {
                 split_contributors(uint64_t(tile - sch.sk_tile0), KB, G, sch.sk_total, c_first, c_end);
-                const uint64_t off = uint64_t(row) * 16;
-                const int4* cell0 = reinterpret_cast<const int4*>(
-                    p.parts + uint64_t(c_first) * (kMaxBN * kTileN) + off);
-                const int4* cell1 = reinterpret_cast<const int4*>(
-                    p.parts + uint64_t(c_first + 1 < c_end ? c_first + 1 : c_first) * (kMaxBN * kTileN) + off);
-#pragma unroll
-                for (uint32_t q = 0; q < 4; ++q) {
-                    pre0[q] = __ldcg(cell0 + q);
-                    pre1[q] = __ldcg(cell1 + q);
-                }
+                load_batch(c_first, 0);
             }
             asm volatile("bar.sync 1, 128;" ::: "memory");
             ptx::mbar_wait(accfull_bar(as), acc_ph);
@@ -676,35 +683,18 @@ __global__ void __launch_bounds__(kThreads, kDecode ? 2 : 1)
                     int32_t sum[16];
 #pragma unroll
                     for (uint32_t j = 0; j < 16; ++j) sum[j] = int32_t(v[j]);
-                    const uint64_t off = uint64_t(ch * kTileN + row) * 16;
-                    for (uint32_t c = c_first; c < c_end; c += 2) {
-                        const bool two = c + 1 < c_end;
-                        int4* cell0 = reinterpret_cast<int4*>(p.parts + uint64_t(c) * (kMaxBN * kTileN) + off);
-                        int4* cell1 = reinterpret_cast<int4*>(p.parts + uint64_t(two ? c + 1 : c) * (kMaxBN * kTileN) + off);
-                        int4 a0[4], a1[4];
-                        if (c == c_first) {
-                            // cells of this chunk were requested one chunk ago (or
-                            // before the accumulator wait); request the next chunk's
-                            // now, so the round trips overlap (software pipeline).
-#pragma unroll
-                            for (uint32_t q = 0; q < 4; ++q) {
-                                a0[q] = pre0[q];
-                                a1[q] = pre1[q];
-                            }
-                            if (!(kDecode && LQG_DECODE_NOPIPE) && ch + 1 < nchunks) {
-#pragma unroll
-                                for (uint32_t q = 0; q < 4; ++q) {
-                                    pre0[q] = __ldcg(cell0 + 4 * kTileN + q);
-                                    pre1[q] = __ldcg(cell1 + 4 * kTileN + q);
-                                }
-                            }
-                        } else {
-#pragma unroll
-                            for (uint32_t q = 0; q < 4; ++q) {
-                                a0[q] = __ldcg(cell0 + q);
-                                a1[q] = __ldcg(cell1 + q);
-                            }
-                        }
+                    // Contributors in batches of four: all of a batch's cells are
+                    // requested together, so the usual case (<= 4 contributors)
+                    // costs at most one L2 round trip per chunk, and the first
+                    // batch of the next chunk is requested before this chunk's
+                    // stores (software pipeline across chunks).
+                    for (uint32_t c = c_first; c < c_end; c += 4) {
+                        const uint32_t nb = min(4u, c_end - c);
+                        if (c != c_first) load_batch(c, ch);
+                        const int32_t* base = parts_row + uint64_t(c) * (kMaxBN * kTileN) + uint64_t(ch) * kTileN * 16;
+                        auto cell = [&](uint32_t b) {
+                            return reinterpret_cast<int4*>(const_cast<int32_t*>(base) + uint64_t(b) * (kMaxBN * kTileN));
+                        };
                         // re-read, in one batch, every int4 that still holds the sentinel
                         auto pend = [](const int4& x) {
                             return x.x == INT32_MIN || x.y == INT32_MIN || x.z == INT32_MIN ||
@@ -714,36 +704,35 @@ __global__ void __launch_bounds__(kThreads, kDecode ? 2 : 1)
                         for (;;) {
                             uint32_t mask = 0;
 #pragma unroll
-                            for (uint32_t q = 0; q < 4; ++q) {
-                                mask |= pend(a0[q]) ? (1u << q) : 0u;
-                                mask |= (two && pend(a1[q])) ? (16u << q) : 0u;
-                            }
+                            for (uint32_t b = 0; b < 4; ++b)
+#pragma unroll
+                                for (uint32_t q = 0; q < 4; ++q)
+                                    mask |= (b < nb && pend(cb[b][q])) ? (1u << (4 * b + q)) : 0u;
                             if (spins == 0 && et == 0 && c == c_first) LQG_T(12);
                             if (!mask) break;
                             ++spins;
-                            __nanosleep(64);
+                            __nanosleep(32);
 #pragma unroll
-                            for (uint32_t q = 0; q < 4; ++q) {
-                                if (mask & (1u << q)) a0[q] = ptx::ld_relaxed_v4(cell0 + q);
-                                if (mask & (16u << q)) a1[q] = ptx::ld_relaxed_v4(cell1 + q);
-                            }
+                            for (uint32_t b = 0; b < 4; ++b)
+#pragma unroll
+                                for (uint32_t q = 0; q < 4; ++q)
+                                    if (mask & (1u << (4 * b + q))) cb[b][q] = ptx::ld_relaxed_v4(cell(b) + q);
                         }
                         if (et == 0 && c == c_first) LQG_TV(13, spins);
 #pragma unroll
-                        for (uint32_t q = 0; q < 4; ++q) {
-                            sum[4 * q] += a0[q].x;
-                            sum[4 * q + 1] += a0[q].y;
-                            sum[4 * q + 2] += a0[q].z;
-                            sum[4 * q + 3] += a0[q].w;
-                            __stcg(cell0 + q, make_int4(INT32_MIN, INT32_MIN, INT32_MIN, INT32_MIN));
-                            if (two) {
-                                sum[4 * q] += a1[q].x;
-                                sum[4 * q + 1] += a1[q].y;
-                                sum[4 * q + 2] += a1[q].z;
-                                sum[4 * q + 3] += a1[q].w;
-                                __stcg(cell1 + q, make_int4(INT32_MIN, INT32_MIN, INT32_MIN, INT32_MIN));
+                        for (uint32_t b = 0; b < 4; ++b) {
+                            if (b < nb) {
+#pragma unroll
+                                for (uint32_t q = 0; q < 4; ++q) {
+                                    sum[4 * q] += cb[b][q].x;
+                                    sum[4 * q + 1] += cb[b][q].y;
+                                    sum[4 * q + 2] += cb[b][q].z;
+                                    sum[4 * q + 3] += cb[b][q].w;
+                                    __stcg(cell(b) + q, make_int4(INT32_MIN, INT32_MIN, INT32_MIN, INT32_MIN));
+                                }
                             }
                         }
+                        if (c + 4 >= c_end && ch + 1 < nchunks) load_batch(c_first, ch + 1);
                     }
                     if (ch == 0 && et == 0) LQG_T(10);
                     if (n < p.N) store_chunk(p, m0 + ch * 16, n, sum, cs, ts_s + ch * 16);
