@@ -17,7 +17,6 @@
 #include "../../include/lqg.h"
 #include "lqg_aux.cuh"
 #include "lqg_gemm.cuh"
-#include "lqg_gemm_dyn.cuh"
 #include "lqg_layout.h"
 
 using namespace lqg;
@@ -100,7 +99,6 @@ constexpr uint64_t kSlotCells = 256ull * kTileN;  // INT32 partial-sum cells per
 struct lqg_workspace {
     int device = 0;
     int32_t* parts = nullptr;  // [kMaxSlots][kSlotCells], INT32_MIN = not published
-    uint32_t* dcnt = nullptr;  // dynamic schedule: claim counter, zero between launches
 };
 
 struct lqg_weights {
@@ -130,13 +128,7 @@ int workspace_create(int dev, lqg_workspace** out) {
         delete w;
         return set_err(LQG_ECUDA, "workspace allocation failed");
     }
-    if (cudaMalloc(&w->dcnt, 256) != cudaSuccess) {
-        cudaFree(w->parts);
-        delete w;
-        return set_err(LQG_ECUDA, "workspace allocation failed");
-    }
     fill_i32_kernel<<<592, 256>>>(w->parts, kMaxSlots * kSlotCells, INT32_MIN);
-    fill_i32_kernel<<<1, 64>>>(reinterpret_cast<int32_t*>(w->dcnt), 64, 0);
     if (cudaDeviceSynchronize() != cudaSuccess) return set_err(LQG_ECUDA, "workspace memset failed");
     *out = w;
     return LQG_OK;
@@ -425,37 +417,7 @@ int launch_gemm(const lqg_weights* w, const int8_t* d_x, int64_t ldx, const floa
         if (uint32_t e = env_u32("LQG_DEBUG_RASTER_GM", 0)) gm = e;
         p.raster_gm = std::max(1u, std::min(gm, MT));
     }
-    // Dynamic schedule (lqg_gemm_dyn.cuh) for one small token tile: k-major
-    // units of unit_kb k-blocks, ~LQG_DYN_UNITS_PER_SM units per SM, at most
-    // kDynMaxUPT units per tile, partials of every unit resident in `parts`.
-    bool dyn = MT == 1 && BN <= kDynMaxBN && env_u32("LQG_DYN", 0);
-    uint32_t dyn_grid = 0;
-    if (dyn) {
-        const uint64_t chunks = uint64_t(G.NT) * G.KB;
-        const uint64_t target = uint64_t(env_u32("LQG_DYN_UNITS_PER_SM", 8)) * w->num_sms;
-        uint32_t u = static_cast<uint32_t>(std::max<uint64_t>(1, (chunks + target - 1) / target));
-        if (uint32_t e = env_u32("LQG_DYN_UNIT_KB", 0)) u = e;
-        u = std::max(u, (G.KB + kDynMaxUPT - 1) / kDynMaxUPT);
-        const uint64_t capacity = kMaxSlots * kSlotCells;
-        for (;;) {
-            u = std::min(u, G.KB);
-            const uint32_t upt = (G.KB + u - 1) / u;
-            p.unit_kb = (G.KB + upt - 1) / upt;  // balanced units
-            p.units_per_tile = (G.KB + p.unit_kb - 1) / p.unit_kb;
-            const uint64_t n_units = uint64_t(G.NT) * p.units_per_tile;
-            if (p.units_per_tile == 1 || n_units * BN * kTileN <= capacity) break;
-            ++u;
-        }
-        const uint64_t n_units = uint64_t(G.NT) * p.units_per_tile;
-        dyn_grid = static_cast<uint32_t>(std::min<uint64_t>(std::min<uint32_t>(w->num_sms, kMaxSlots), n_units));
-        p.static_units = static_cast<uint32_t>(std::min<uint64_t>(n_units, 2ull * dyn_grid));
-        p.dcnt = W->dcnt;
-        p.stages = std::min<uint32_t>(kMaxStages, (227 * 1024 - 1024 - kDynCtlBytes) / p.stage_bytes);
-        if (uint32_t st = env_u32("LQG_DEBUG_STAGES", 0)) p.stages = std::min(p.stages, st);
-        if (n_units >= (uint64_t(1) << 31)) dyn = false;
-    }
-    const size_t smem = dyn ? size_t(p.stages) * p.stage_bytes + 1024 + kDynCtlBytes
-                            : size_t(p.stages) * p.stage_bytes + 1024 + 2048;
+    const size_t smem = size_t(p.stages) * p.stage_bytes + 1024 + 2048;
 
     DeviceGuard dg(w->device);
     cudaError_t e = cudaSuccess;
@@ -465,13 +427,10 @@ int launch_gemm(const lqg_weights* w, const int8_t* d_x, int64_t ldx, const floa
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(lqg_w4a8_gemm_kernel<false>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(lqg_w4a8_dyn_kernel,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     });
     if (e != cudaSuccess) return set_err(LQG_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(dyn ? dyn_grid : grid);
+    cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
@@ -480,9 +439,7 @@ int launch_gemm(const lqg_weights* w, const int8_t* d_x, int64_t ldx, const floa
     attr[0].val.programmaticStreamSerializationAllowed = env_u32("LQG_DEBUG_NO_PDL", 0) ? 0 : 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (dyn)
-        LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_dyn_kernel, tmap, p));
-    else if (decode)
+    if (decode)
         LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<true>, tmap, p));
     else
         LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<false>, tmap, p));
@@ -731,7 +688,6 @@ int lqg_workspace_destroy(lqg_workspace* ws) {
     if (!ws) return LQG_OK;
     DeviceGuard g(ws->device);
     cudaFree(ws->parts);
-    cudaFree(ws->dcnt);
     delete ws;
     return LQG_OK;
 }

@@ -103,11 +103,6 @@ struct GemmParams {
     uint32_t pdl_trigger;
     uint32_t prewait_stages;   // weight chunks requested before griddepcontrol.wait      // 0: after the prologue, 1: after the last load is issued, 2: after the last MMA
     uint64_t total_iters;      // MT*NT*KB
-    // dynamic (work-stealing) decode schedule, lqg_gemm_dyn.cuh
-    uint32_t unit_kb;          // k-blocks per work unit
-    uint32_t units_per_tile;   // ceil(KB / unit_kb)
-    uint32_t static_units;     // units [0, static_units) are assigned round-robin, the rest claimed
-    uint32_t* dcnt;            // claim counter, zero between launches
 };
 
 // LiquidQuant dequantization of one interleaved word (packed.cpp:63-71):

@@ -75,50 +75,6 @@ __device__ __forceinline__ int4 ld_relaxed_v4(const int4* addr) {
     return v;
 }
 
-// INT32 add at GPU scope without a return value (RED): split-K partials.
-__device__ __forceinline__ void red_add_s32(int32_t* addr, int32_t v) {
-    asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(addr), "r"(v) : "memory");
-}
-// Acquire-release counter increment at GPU scope; returns the old value.
-__device__ __forceinline__ uint32_t atom_add_acq_rel_u32(uint32_t* addr, uint32_t v) {
-    uint32_t old;
-    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(addr), "r"(v) : "memory");
-    return old;
-}
-
-// ---------------------------------------------------------------- cluster launch control
-// Hardware work stealing (sm_100): ask the scheduler to cancel one not-yet-
-// launched CTA of this grid; the 16-byte response lands in shared memory with
-// complete_tx(16) on `bar`. Must not be re-issued after a failed response.
-__device__ __forceinline__ void clc_try_cancel(uint32_t result_smem, uint32_t bar) {
-    asm volatile(
-        "clusterlaunchcontrol.try_cancel.async.shared::cta.mbarrier::complete_tx::bytes.b128 [%0], [%1];" ::"r"(
-            result_smem),
-        "r"(bar)
-        : "memory");
-}
-// ctaid.x of the CTA the response cancelled (its work is now ours), or
-// 0xFFFFFFFF when no unlaunched CTA was left.
-__device__ __forceinline__ uint32_t clc_query(uint32_t result_smem) {
-    uint32_t x = 0, valid = 0;
-    asm volatile(
-        "{\n\t.reg .pred p1;\n\t.reg .b128 r;\n\t"
-        "ld.shared.b128 r, [%2];\n\t"
-        "clusterlaunchcontrol.query_cancel.is_canceled.pred.b128 p1, r;\n\t"
-        "selp.u32 %1, 1, 0, p1;\n\t"
-        "@p1 clusterlaunchcontrol.query_cancel.get_first_ctaid::x.b32.b128 %0, r;\n\t}"
-        : "+r"(x), "=r"(valid)
-        : "r"(result_smem)
-        : "memory");
-    return valid ? x : 0xFFFFFFFFu;
-}
-
-__device__ __forceinline__ int32_t ld_relaxed_s32(const int32_t* addr) {
-    int32_t v;
-    asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(addr) : "memory");
-    return v;
-}
-
 // ---------------------------------------------------------------- L2 policies
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;
