@@ -431,7 +431,7 @@ int launch_gemm(const lqg_weights* w, const int8_t* d_x, int64_t ldx, const floa
     if (e != cudaSuccess) return set_err(LQG_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(decode ? Roles<true>::kThreadsT : Roles<false>::kThreadsT);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];

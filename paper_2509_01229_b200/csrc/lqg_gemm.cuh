@@ -51,12 +51,20 @@ namespace lqg {
 
 enum OutKind : uint32_t { kOutAcc = 0, kOutF32 = 1, kOutF16 = 2, kOutBF16 = 3 };
 
-// Warp roles: 0 TMA producer, 1 MMA issuer (+ TMEM alloc), 2-9 dequant,
-// 10-13 epilogue. 448 threads so that two co-resident CTAs (decode mode) get
-// 72 registers per thread.
+// Warp roles: 0 TMA producer, 1 MMA issuer (+ TMEM alloc), then the dequant
+// warpgroups, then 4 epilogue warps. One CTA per SM: two dequant WGs (448
+// threads). Co-resident decode mode (two CTAs per SM): one dequant WG (320
+// threads, so each CTA keeps ~100 registers per thread) -- at BN <= 32 one WG
+// dequantizes a k-block several times faster than HBM delivers it.
 constexpr uint32_t kThreads = 448;
 constexpr uint32_t kDequantWarp0 = 2;
 constexpr uint32_t kEpiWarp0 = 10;
+template <bool kDecode>
+struct Roles {
+    static constexpr uint32_t kDQWarps = kDecode ? 4 : 8;
+    static constexpr uint32_t kEpi0 = kDequantWarp0 + kDQWarps;
+    static constexpr uint32_t kThreadsT = (kEpi0 + 4) * 32;
+};
 constexpr uint32_t kMaxStages = 16;
 constexpr uint32_t kMaxASlots = 8;
 constexpr uint32_t kACols = kKBlock / 4;   // TMEM columns per A slot (4 int8 per column)
@@ -276,7 +284,7 @@ __device__ __forceinline__ void trace(uint32_t slot, uint32_t e) {
 // kDecode: two CTAs per SM (<= 110 KB SMEM, 256 TMEM columns, <= 72 registers)
 // so consecutive GEMMs overlap under PDL; otherwise one CTA per SM.
 template <bool kDecode>
-__global__ void __launch_bounds__(kThreads, kDecode ? 2 : 1)
+__global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
     lqg_w4a8_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const GemmParams p) {
     extern __shared__ uint8_t smem_raw[];
     // 1024-byte alignment for the SW128 activation tiles.
@@ -317,7 +325,7 @@ __global__ void __launch_bounds__(kThreads, kDecode ? 2 : 1)
             ptx::mbar_init(empty_bar(s), 1);
         }
         for (uint32_t a = 0; a < kMaxASlots; ++a) {
-            ptx::mbar_init(afull_bar(a), 8);  // one arrive per dequant warp (both WGs)
+            ptx::mbar_init(afull_bar(a), Roles<kDecode>::kDQWarps);  // one arrive per dequant warp
             ptx::mbar_init(aempty_bar(a), 1);
         }
         for (uint32_t a = 0; a < 2; ++a) {
@@ -494,17 +502,17 @@ __global__ void __launch_bounds__(kThreads, kDecode ? 2 : 1)
             }
         }
         if (lane == 0 && p.pdl_trigger == 2) ptx::launch_dependents();
-    } else if (warp >= kDequantWarp0 && warp < kEpiWarp0) {
+    } else if (warp >= kDequantWarp0 && warp < Roles<kDecode>::kEpi0) {
         // ------------------------------------------------------------ dequant WGs
         // Both warpgroups work on every k-block: WG w dequantizes sub-blocks
         // [4w, 4w+4). Every waiter therefore observes every phase of every
         // ring barrier (a parity wait can never alias an older phase).
-        const uint32_t wg = (warp - kDequantWarp0) / 4;  // 0 or 1: which half of the k-block
+        const uint32_t wg = (warp - kDequantWarp0) / 4;  // which part of the k-block
         const uint32_t sp = warp % 4;            // TMEM sub-partition
         const uint32_t row = sp * 32 + lane;     // weight row within the tile = TMEM lane
         const uint32_t lane_addr = (sp * 32) << 16;
         const uint32_t p_shift = param_shift(p.P);
-        constexpr uint32_t kHalf = kSubBlocks / 2;
+        constexpr uint32_t kHalf = kSubBlocks / (Roles<kDecode>::kDQWarps / 4);  // sub-blocks per WG
         uint32_t s = 0, ph = 0, a = 0, aph = 0;
         const uint8_t* ring_w = smem + x_bytes;
         const uint32_t a_base = tmem_base + lane_addr + tp.a_base + wg * kHalf * 8;
@@ -553,12 +561,12 @@ __global__ void __launch_bounds__(kThreads, kDecode ? 2 : 1)
                 aph ^= 1;
             }
         }
-    } else if (warp >= kEpiWarp0) {
+    } else if (warp >= Roles<kDecode>::kEpi0) {
         // ------------------------------------------------------------ epilogue
         const uint32_t sp = warp % 4;
         const uint32_t row = sp * 32 + lane;
         const uint32_t lane_addr = (sp * 32) << 16;
-        const uint32_t et = threadIdx.x - kEpiWarp0 * 32;  // 0..127
+        const uint32_t et = threadIdx.x - Roles<kDecode>::kEpi0 * 32;  // 0..127
         const uint32_t nchunks = p.BN / 16;
         const bool scaled = p.out_kind != kOutAcc;
         ptx::griddep_wait();
@@ -737,7 +745,7 @@ __global__ void __launch_bounds__(kThreads, kDecode ? 2 : 1)
         }
     }
 
-    if (warp == kEpiWarp0 && lane == 0) LQG_T(7);
+    if (warp == Roles<kDecode>::kEpi0 && lane == 0) LQG_T(7);
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
