@@ -155,6 +155,25 @@ int lqg_gemm_w4a8(const lqg_weights* w, const int8_t* d_x, int64_t ldx,
 int lqg_gemm_w4a8_accum(const lqg_weights* w, const int8_t* d_x, int64_t ldx, uint32_t m,
                         int32_t* d_acc, int64_t ldacc, lqg_workspace* ws, void* stream);
 
+/* Grouped (MoE) W4A8 GEMM: num_groups problems that share n, k and group size
+ * (the experts of one layer, BASELINE config 5 / the paper's MoE case, P:615,
+ * P:618) in ONE persistent launch -- stream-K over the union of all groups'
+ * tiles, so small experts do not each pay a launch and a tail. Group e owns
+ * the m[e] rows starting at row0_e = m[0] + ... + m[e-1] of d_x (int8 codes,
+ * pitch ldx), d_token_scales and d_y (pitch ldy): the expert-sorted token
+ * layout. m[e] may be 0. weights[e] are handles on the same device.
+ * Per group the result is bit-identical to lqg_gemm_w4a8 on that group alone
+ * (and hence to the reference's gemm_w4a8, gemm.cpp:213-223).
+ * 1 <= num_groups <= 64. */
+int lqg_gemm_w4a8_grouped(const lqg_weights* const* weights, uint32_t num_groups,
+                          const int8_t* d_x, int64_t ldx, const float* d_token_scales,
+                          const uint32_t* m, void* d_y, int64_t ldy, int y_dtype,
+                          lqg_workspace* ws, void* stream);
+/* INT32 accumulators of the grouped GEMM (gemm.cpp:138-211 per group). */
+int lqg_gemm_w4a8_grouped_accum(const lqg_weights* const* weights, uint32_t num_groups,
+                                const int8_t* d_x, int64_t ldx, const uint32_t* m,
+                                int32_t* d_acc, int64_t ldacc, lqg_workspace* ws, void* stream);
+
 /* Host-buffer call with the reference's convention: x is m*k int8 codes
  * (row-major, ActivationQuant::values, gemm.hpp:35-39), token_scales m floats,
  * y receives m*n values of y_dtype, row-major. Stages through device buffers

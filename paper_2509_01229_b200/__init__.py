@@ -12,14 +12,15 @@ or no sm_100 device is present.
 from . import _lib
 from .lq import (ActivationQuant, CudaError, DeviceWeights, Engine, FragmentDescriptor, GemmShape,
                  IoError, QuantizedWeightBundle, TileConfig, UnsupportedDeviceError,
-                 ValidationError, VerificationError, WeightLayout, Workspace, gemm_w4a8,
-                 gemm_w4a8_accum, launch_count, quantize_activations,
+                 ValidationError, VerificationError, WeightLayout, Workspace, gemm_grouped,
+                 gemm_grouped_accum, gemm_w4a8, gemm_w4a8_accum, launch_count, quantize_activations,
                  quantize_activations_per_token)
 
 __all__ = [
     "ActivationQuant", "CudaError", "DeviceWeights", "Engine", "FragmentDescriptor", "GemmShape",
     "IoError", "QuantizedWeightBundle", "TileConfig", "UnsupportedDeviceError", "ValidationError",
-    "VerificationError", "WeightLayout", "Workspace", "gemm_w4a8", "gemm_w4a8_accum",
+    "VerificationError", "WeightLayout", "Workspace", "gemm_grouped", "gemm_grouped_accum",
+    "gemm_w4a8", "gemm_w4a8_accum",
     "launch_count", "quantize_activations", "quantize_activations_per_token", "build",
 ]
 

@@ -88,6 +88,8 @@ def lib() -> C.CDLL:
         "lqg_workspace_destroy": [vp],
         "lqg_gemm_w4a8": [vp, vp, i64, vp, u32, vp, i64, i32, vp, vp],
         "lqg_gemm_w4a8_accum": [vp, vp, i64, u32, vp, i64, vp, vp],
+        "lqg_gemm_w4a8_grouped": [vp, u32, vp, i64, vp, vp, vp, i64, i32, vp, vp],
+        "lqg_gemm_w4a8_grouped_accum": [vp, u32, vp, i64, vp, vp, i64, vp, vp],
         "lqg_gemm_w4a8_host": [vp, vp, vp, u32, vp, i32, vp],
         "lqg_gemm_w4a8_accum_host": [vp, vp, u32, vp, vp],
         "lqg_dequant_weights": [vp, vp, i64, vp],
@@ -114,6 +116,7 @@ EXPORTS = [
     "lqg_weights_create", "lqg_weights_quantize", "lqg_weights_destroy",
     "lqg_weights_shape", "lqg_weights_export", "lqg_weights_device_bytes",
     "lqg_workspace_create", "lqg_workspace_destroy", "lqg_gemm_w4a8", "lqg_gemm_w4a8_accum",
+    "lqg_gemm_w4a8_grouped", "lqg_gemm_w4a8_grouped_accum",
     "lqg_gemm_w4a8_host", "lqg_gemm_w4a8_accum_host", "lqg_dequant_weights",
     "lqg_quantize_activations", "lqg_kernel_launch_count", "lqg_last_error", "lqg_version",
 ]

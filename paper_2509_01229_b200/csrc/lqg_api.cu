@@ -324,10 +324,29 @@ uint32_t choose_bn(uint32_t m, uint32_t* mt) {
 
 std::once_flag g_attr_once[64];
 
-int launch_gemm(const lqg_weights* w, const int8_t* d_x, int64_t ldx, const float* d_ts, uint32_t m,
-                void* d_out, int64_t ldo, uint32_t out_kind, lqg_workspace* ws, cudaStream_t stream) {
+constexpr uint32_t kMaxGroups = 64;  // experts per grouped launch
+
+// One launch over `ng` weight groups sharing n, k and group size (ng == 1: a
+// plain GEMM). Group e owns rows [row0_e, row0_e + m[e]) of X, token scales
+// and Y, concatenated in group order.
+int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* m_list,
+                const int8_t* d_x, int64_t ldx, const float* d_ts, void* d_out, int64_t ldo,
+                uint32_t out_kind, lqg_workspace* ws, cudaStream_t stream) {
+    const lqg_weights* w = ws_list[0];
     const ImageGeom& G = w->geom;
-    if (m < 1) return set_err(LQG_EVALIDATION, "activation dimensions must be >= 1");
+    uint64_t rows = 0;
+    uint32_t max_m = 0;
+    for (uint32_t e = 0; e < ng; ++e) {
+        const lqg_weights* we = ws_list[e];
+        if (!we) return set_err(LQG_EVALIDATION, "null handle");
+        if (we->geom.n != G.n || we->geom.k != G.k || we->geom.g != G.g || we->device != w->device)
+            return set_err(LQG_EVALIDATION, "grouped weights must share n, k, group_size and device");
+        rows += m_list[e];
+        max_m = std::max(max_m, m_list[e]);
+    }
+    if (rows < 1) return set_err(LQG_EVALIDATION, "activation dimensions must be >= 1");
+    if (rows >= (uint64_t(1) << 31)) return set_err(LQG_EVALIDATION, "too many activation rows");
+    const uint32_t m = static_cast<uint32_t>(rows);
     if (int64_t(G.k) * 127 * 127 >= (int64_t(1) << 31))
         return set_err(LQG_EVALIDATION, "k = " + std::to_string(G.k) +
                                             " risks 32-bit accumulator overflow (k*127*127 >= 2^31)");
@@ -343,8 +362,9 @@ int launch_gemm(const lqg_weights* w, const int8_t* d_x, int64_t ldx, const floa
     EncodeTiledFn enc = encode_fn();
     if (!enc) return set_err(LQG_ECUDA, "cuTensorMapEncodeTiled unavailable");
 
+    // Token tile from the largest group; every group gets ceil(m_e / BN) tiles.
     uint32_t MT;
-    const uint32_t BN = choose_bn(m, &MT);
+    const uint32_t BN = choose_bn(max_m, &MT);
     CUtensorMap tmap;
     const cuuint64_t dims[2] = {G.k, m};
     const cuuint64_t strides[1] = {cuuint64_t(ldx)};
@@ -357,30 +377,43 @@ int launch_gemm(const lqg_weights* w, const int8_t* d_x, int64_t ldx, const floa
     if (cr != CUDA_SUCCESS)
         return set_err(LQG_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(int(cr)) + ")");
 
+    GroupTable<kMaxGroups> gt{};
+    uint32_t tiles = 0, row0 = 0;
+    for (uint32_t e = 0; e < ng; ++e) {
+        GroupEntry& ge = gt.e[e];
+        ge.wimg = ws_list[e]->d_img;
+        ge.cs = ws_list[e]->d_cs;
+        ge.row0 = row0;
+        ge.M = m_list[e];
+        ge.MT = (m_list[e] + BN - 1) / BN;
+        ge.tile0 = tiles;
+        tiles += ge.MT * G.NT;
+        row0 += m_list[e];
+    }
+    gt.n = ng;
+
     GemmParams p{};
-    p.wimg = w->d_img;
-    p.cs = w->d_cs;
     p.ts = d_ts;
     p.out = d_out;
     p.ldo = ldo;
     p.parts = W->parts;
-    p.M = m;
     p.N = G.n;
     p.KB = G.KB;
     p.NT = G.NT;
-    p.MT = MT;
+    p.MT = MT;  // token tiles of the largest group
+    p.tiles = tiles;
     p.BN = BN;
     p.P = G.P;
     p.chunk_bytes = G.chunk_bytes;
     p.out_kind = out_kind;
     p.stage_bytes = (BN * kKBlock + G.chunk_bytes + 1023) / 1024 * 1024;
-    // Co-resident mode (opt-in, LQG_CORESIDENT=1, small token tiles only): <= 110
-    // KB of shared memory and 256 TMEM columns so that two CTAs fit on an SM
-    // and the next GEMM's CTAs are resident while this one drains. Measured on
-    // B200 it loses to one CTA per SM with the full 227 KB ring (LLaMA-2-70B
-    // 4-layer step at M = 16: 93.9 vs 83.5 us): the halved ring and the
-    // 72-register cap slow the mainloop more than the earlier start gains.
-    const bool decode = BN <= kDecodeMaxBN && env_u32("LQG_CORESIDENT", 0);
+    // Co-resident mode (opt-in, LQG_CORESIDENT=1, single group, small token
+    // tiles): <= 110 KB of shared memory, 256 TMEM columns and one dequant
+    // warpgroup so that two CTAs fit on an SM and the next GEMM's CTAs are
+    // resident while this one drains. Measured on B200 it loses to one CTA per
+    // SM with the full 227 KB ring (LLaMA-2-70B 4-layer step at M = 16: 95 vs
+    // 81 us): the halved ring slows the mainloop more than the earlier start gains.
+    const bool decode = ng == 1 && BN <= kDecodeMaxBN && env_u32("LQG_CORESIDENT", 0);
     p.tmem_cols = decode ? 256 : 512;
     // ~24 MB of weights across the grid (enough to cover a kernel tail at HBM rate).
     p.l2_prefetch = env_u32("LQG_L2_PREFETCH_CHUNKS", decode ? 4 : 0);
@@ -394,7 +427,7 @@ int launch_gemm(const lqg_weights* w, const int8_t* d_x, int64_t ldx, const floa
     if (p.stages < 2) return set_err(LQG_EVALIDATION, "tile configuration does not fit shared memory");
     if (tmem_plan(BN, p.tmem_cols).a_slots < 1)
         return set_err(LQG_EVALIDATION, "tile configuration does not fit tensor memory");
-    p.total_iters = uint64_t(MT) * G.NT * G.KB;
+    p.total_iters = uint64_t(tiles) * G.KB;
     if (p.total_iters * kMaxSlots >= (uint64_t(1) << 32))
         return set_err(LQG_EVALIDATION, "problem too large for one launch (tiles x k-blocks x " +
                                             std::to_string(kMaxSlots) + " >= 2^32)");
@@ -407,7 +440,7 @@ int launch_gemm(const lqg_weights* w, const int8_t* d_x, int64_t ldx, const floa
     // of GM token tiles sized so that the activation and weight slices of one
     // round balance in L2 (GM^2 ~ G * weight bytes per tile / activation bytes).
     {
-        const uint64_t T = uint64_t(MT) * G.NT;
+        const uint64_t T = tiles;
         uint32_t dp = 0;
         if (!decode && T >= grid && !env_u32("LQG_DEBUG_NO_DP", 0))
             dp = static_cast<uint32_t>(T % grid == 0 ? T / grid : T / grid - 1);
@@ -422,10 +455,13 @@ int launch_gemm(const lqg_weights* w, const int8_t* d_x, int64_t ldx, const floa
     DeviceGuard dg(w->device);
     cudaError_t e = cudaSuccess;
     std::call_once(g_attr_once[w->device % 64], [&] {
-        e = cudaFuncSetAttribute(lqg_w4a8_gemm_kernel<true>,
+        e = cudaFuncSetAttribute(lqg_w4a8_gemm_kernel<true, 1>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(lqg_w4a8_gemm_kernel<false>,
+            e = cudaFuncSetAttribute(lqg_w4a8_gemm_kernel<false, 1>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(lqg_w4a8_gemm_kernel<false, kMaxGroups>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     });
     if (e != cudaSuccess) return set_err(LQG_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
@@ -439,13 +475,26 @@ int launch_gemm(const lqg_weights* w, const int8_t* d_x, int64_t ldx, const floa
     attr[0].val.programmaticStreamSerializationAllowed = env_u32("LQG_DEBUG_NO_PDL", 0) ? 0 : 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (decode)
-        LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<true>, tmap, p));
-    else
-        LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<false>, tmap, p));
+    if (ng > 1) {
+        LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<false, kMaxGroups>, tmap, p, gt));
+    } else {
+        GroupTable<1> g1{};
+        g1.e[0] = gt.e[0];
+        g1.n = 1;
+        if (decode)
+            LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<true, 1>, tmap, p, g1));
+        else
+            LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<false, 1>, tmap, p, g1));
+    }
     g_launches.fetch_add(1, std::memory_order_relaxed);
     LQG_CUDA(cudaGetLastError());
     return LQG_OK;
+}
+
+int launch_gemm(const lqg_weights* w, const int8_t* d_x, int64_t ldx, const float* d_ts, uint32_t m,
+                void* d_out, int64_t ldo, uint32_t out_kind, lqg_workspace* ws, cudaStream_t stream) {
+    if (m < 1) return set_err(LQG_EVALIDATION, "activation dimensions must be >= 1");
+    return launch_core(&w, 1, &m, d_x, ldx, d_ts, d_out, ldo, out_kind, ws, stream);
 }
 
 int ensure_cap(void** ptr, size_t* cap, size_t need) {
@@ -699,6 +748,29 @@ int lqg_gemm_w4a8(const lqg_weights* w, const int8_t* d_x, int64_t ldx, const fl
     int rc = out_kind_of(y_dtype, &kind);
     if (rc) return rc;
     return launch_gemm(w, d_x, ldx, d_ts, m, d_y, ldy, kind, ws, static_cast<cudaStream_t>(stream));
+}
+
+int lqg_gemm_w4a8_grouped(const lqg_weights* const* weights, uint32_t num_groups, const int8_t* d_x,
+                          int64_t ldx, const float* d_token_scales, const uint32_t* m, void* d_y,
+                          int64_t ldy, int y_dtype, lqg_workspace* ws, void* stream) {
+    if (!weights || !m) return set_err(LQG_EVALIDATION, "null argument");
+    if (num_groups < 1 || num_groups > kMaxGroups)
+        return set_err(LQG_EVALIDATION, "num_groups must be in [1, " + std::to_string(kMaxGroups) + "]");
+    uint32_t kind;
+    int rc = out_kind_of(y_dtype, &kind);
+    if (rc) return rc;
+    return launch_core(weights, num_groups, m, d_x, ldx, d_token_scales, d_y, ldy, kind, ws,
+                       static_cast<cudaStream_t>(stream));
+}
+
+int lqg_gemm_w4a8_grouped_accum(const lqg_weights* const* weights, uint32_t num_groups,
+                                const int8_t* d_x, int64_t ldx, const uint32_t* m, int32_t* d_acc,
+                                int64_t ldacc, lqg_workspace* ws, void* stream) {
+    if (!weights || !m) return set_err(LQG_EVALIDATION, "null argument");
+    if (num_groups < 1 || num_groups > kMaxGroups)
+        return set_err(LQG_EVALIDATION, "num_groups must be in [1, " + std::to_string(kMaxGroups) + "]");
+    return launch_core(weights, num_groups, m, d_x, ldx, nullptr, d_acc, ldacc, kOutAcc, ws,
+                       static_cast<cudaStream_t>(stream));
 }
 
 int lqg_gemm_w4a8_accum(const lqg_weights* w, const int8_t* d_x, int64_t ldx, uint32_t m, int32_t* d_acc,

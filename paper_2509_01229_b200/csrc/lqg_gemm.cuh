@@ -87,15 +87,13 @@ __host__ __device__ inline TmemPlan tmem_plan(uint32_t BN, uint32_t cols) {
 }
 
 struct GemmParams {
-    const uint8_t* wimg;       // prepacked weight image
-    const float* cs;           // channel scales (padded to NT*128)
-    const float* ts;           // token scales (m)
+    const float* ts;           // token scales (all rows)
     void* out;                 // y or acc
     int64_t ldo;               // row pitch of out, in elements
     int32_t* parts;            // split-K partials: per CTA kMaxBN*128 int32 cells,
                                // [chunk][row][16 tokens], INT32_MIN = "not published"
-    uint32_t M, N;             // logical problem (tokens, weight rows)
-    uint32_t KB, NT, MT;       // k-blocks, weight tiles, token tiles
+    uint32_t N;                // weight rows
+    uint32_t KB, NT, MT;       // k-blocks, weight tiles, token tiles (of the largest group)
     uint32_t BN;               // tokens per tile (16..256, multiple of 16)
     uint32_t P;                // group params per k-block (1, 2, 4, 8)
     uint32_t chunk_bytes;      // bytes per (tile, k-block) weight chunk
@@ -110,7 +108,29 @@ struct GemmParams {
     uint32_t trace_slot;       // LQG_TRACE builds: launch index % 8
     uint32_t pdl_trigger;
     uint32_t prewait_stages;   // weight chunks requested before griddepcontrol.wait      // 0: after the prologue, 1: after the last load is issued, 2: after the last MMA
-    uint64_t total_iters;      // MT*NT*KB
+    uint64_t total_iters;      // tiles*KB
+    uint32_t tiles;            // weight-tile x token-tile pairs (summed over groups)
+};
+
+// Grouped launch (MoE experts of one layer: same n, k, group size): the
+// tiles of every group form one linear space, tile-major within a group.
+// Group g owns rows [row0, row0 + M) of X / token scales / Y and tiles
+// [tile0, tile0 + MT * NT). A plain GEMM is the one-group case.
+struct GroupEntry {
+    const uint8_t* wimg;  // prepacked weight image of this group
+    const float* cs;      // its channel scales (padded to NT*128)
+    uint32_t row0, M, MT, tile0;
+};
+template <uint32_t kG>
+struct GroupTable {
+    GroupEntry e[kG];
+    uint32_t n;
+};
+// One tile resolved: its group's weights / scales and its absolute rows.
+struct TileRef {
+    const uint8_t* wimg;
+    const float* cs;
+    uint32_t nt, row0, mlim;  // weight tile, first token row, end of the group's rows
 };
 
 // LiquidQuant dequantization of one interleaved word (packed.cpp:63-71):
@@ -166,7 +186,7 @@ __device__ __forceinline__ Sched make_sched(const GemmParams& p) {
     s.c = blockIdx.x;
     s.dp_rounds = p.dp_rounds;
     s.sk_tile0 = s.dp_rounds * G;
-    s.sk_total = (p.MT * p.NT - s.sk_tile0) * p.KB;
+    s.sk_total = (p.tiles - s.sk_tile0) * p.KB;
     s.sk_beg = range_begin32(s.c, G, s.sk_total);
     s.sk_end = range_begin32(s.c + 1, G, s.sk_total);
     s.sk_tile = s.sk_tile0 + s.sk_beg / p.KB;
@@ -214,9 +234,9 @@ struct Walk {
 };
 
 // linear tile -> (token tile mt, weight tile nt), from the parameter bank
-__device__ __forceinline__ void tile_coords_p(uint32_t t, const GemmParams& p, uint32_t& mt,
-                                              uint32_t& nt) {
-    if (p.MT == 1) {
+__device__ __forceinline__ void tile_coords_p(uint32_t t, uint32_t MT, const GemmParams& p,
+                                              uint32_t& mt, uint32_t& nt) {
+    if (MT == 1) {
         mt = 0;
         nt = t;
         return;
@@ -225,9 +245,26 @@ __device__ __forceinline__ void tile_coords_p(uint32_t t, const GemmParams& p, u
     const uint32_t g = t / per_group;
     const uint32_t w = t - g * per_group;
     const uint32_t m0 = g * p.raster_gm;
-    const uint32_t gm = min(p.raster_gm, p.MT - m0);
+    const uint32_t gm = min(p.raster_gm, MT - m0);
     mt = m0 + w % gm;
     nt = w / gm;
+}
+
+template <uint32_t kG>
+__device__ __forceinline__ TileRef tile_ref(uint32_t t, const GemmParams& p, const GroupTable<kG>& gt) {
+    uint32_t g = 0;
+    if (kG > 1)
+        while (g + 1 < gt.n && t >= gt.e[g + 1].tile0) ++g;
+    const GroupEntry& e = gt.e[g];
+    uint32_t mt, nt;
+    tile_coords_p(t - e.tile0, e.MT, p, mt, nt);
+    TileRef r;
+    r.wimg = e.wimg;
+    r.cs = e.cs;
+    r.nt = nt;
+    r.row0 = e.row0 + mt * p.BN;
+    r.mlim = e.row0 + e.M;
+    return r;
 }
 
 // y = float(double(acc) * double(cs) * double(ts)) (quant.cpp:125-127), left
@@ -235,10 +272,10 @@ __device__ __forceinline__ void tile_coords_p(uint32_t t, const GemmParams& p, u
 // the 16 tokens [m0, m0+16) of output column n; the output kind is a template
 // parameter so every store loop is branch-free (dispatch once per chunk).
 template <uint32_t kKind>
-__device__ __forceinline__ void store_chunk_k(const GemmParams& p, uint32_t m0, uint32_t n,
-                                              const int32_t (&acc)[16], double cs_d,
+__device__ __forceinline__ void store_chunk_k(const GemmParams& p, uint32_t m0, uint32_t mlim,
+                                              uint32_t n, const int32_t (&acc)[16], double cs_d,
                                               const float* ts) {
-    const uint32_t mend = min(16u, p.M > m0 ? p.M - m0 : 0u);
+    const uint32_t mend = min(16u, mlim > m0 ? mlim - m0 : 0u);
     uint64_t idx = uint64_t(m0) * uint64_t(p.ldo) + n;
 #pragma unroll
     for (uint32_t j = 0; j < 16; ++j, idx += p.ldo) {
@@ -257,13 +294,13 @@ __device__ __forceinline__ void store_chunk_k(const GemmParams& p, uint32_t m0, 
     }
 }
 
-__device__ __forceinline__ void store_chunk(const GemmParams& p, uint32_t m0, uint32_t n,
+__device__ __forceinline__ void store_chunk(const GemmParams& p, uint32_t m0, uint32_t mlim, uint32_t n,
                                             const int32_t (&acc)[16], double cs_d, const float* ts) {
     switch (p.out_kind) {
-        case kOutAcc: store_chunk_k<kOutAcc>(p, m0, n, acc, cs_d, ts); break;
-        case kOutF32: store_chunk_k<kOutF32>(p, m0, n, acc, cs_d, ts); break;
-        case kOutF16: store_chunk_k<kOutF16>(p, m0, n, acc, cs_d, ts); break;
-        default: store_chunk_k<kOutBF16>(p, m0, n, acc, cs_d, ts); break;
+        case kOutAcc: store_chunk_k<kOutAcc>(p, m0, mlim, n, acc, cs_d, ts); break;
+        case kOutF32: store_chunk_k<kOutF32>(p, m0, mlim, n, acc, cs_d, ts); break;
+        case kOutF16: store_chunk_k<kOutF16>(p, m0, mlim, n, acc, cs_d, ts); break;
+        default: store_chunk_k<kOutBF16>(p, m0, mlim, n, acc, cs_d, ts); break;
     }
 }
 
@@ -283,9 +320,11 @@ __device__ __forceinline__ void trace(uint32_t slot, uint32_t e) {
 
 // kDecode: two CTAs per SM (<= 110 KB SMEM, 256 TMEM columns, <= 72 registers)
 // so consecutive GEMMs overlap under PDL; otherwise one CTA per SM.
-template <bool kDecode>
+// kG > 1: grouped launch over up to kG weight groups (MoE experts).
+template <bool kDecode, uint32_t kG>
 __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
-    lqg_w4a8_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const GemmParams p) {
+    lqg_w4a8_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const GemmParams p,
+                         const __grid_constant__ GroupTable<kG> gt) {
     extern __shared__ uint8_t smem_raw[];
     // 1024-byte alignment for the SW128 activation tiles.
     const uint32_t raw_addr = ptx::smem_u32(smem_raw);
@@ -361,13 +400,14 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
         // weight walker
         Walk<!kDecode> ww;
         ww.init(sch);
-        uint32_t wmt, wnt;
-        tile_coords_p(ww.tile, p, wmt, wnt);
-        const uint8_t* src = p.wimg + (uint64_t(wnt) * KB + ww.kb) * p.chunk_bytes;
+        auto chunk_src = [&](uint32_t tile, uint32_t kb) {
+            const TileRef r = tile_ref(tile, p, gt);
+            return r.wimg + (uint64_t(r.nt) * KB + kb) * p.chunk_bytes;
+        };
+        const uint8_t* src = chunk_src(ww.tile, ww.kb);
         auto w_next = [&]() {
             if (ww.next(p)) {
-                tile_coords_p(ww.tile, p, wmt, wnt);
-                src = p.wimg + (uint64_t(wnt) * KB + ww.kb) * p.chunk_bytes;
+                src = chunk_src(ww.tile, ww.kb);
             } else {
                 src += p.chunk_bytes;
             }
@@ -381,18 +421,17 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
         // activation walker
         Walk<!kDecode> xw;
         xw.init(sch);
-        uint32_t xmt, xnt;
-        tile_coords_p(xw.tile, p, xmt, xnt);
+        uint32_t xrow0 = tile_ref(xw.tile, p, gt).row0;
         auto x_issue = [&](uint32_t st) {
             const uint32_t slot = smem_base + st * p.stage_bytes;
             ptx::mbar_arrive_expect_tx(xfull_bar(st), x_bytes);
-            const int32_t k0 = int32_t(xw.kb * kKBlock), m0 = int32_t(xmt * p.BN);
+            const int32_t k0 = int32_t(xw.kb * kKBlock), m0 = int32_t(xrow0);
             ptx::tma_2d_g2s(slot, &tmap_x, k0, m0, xfull_bar(st), pol_x);
             ptx::tma_2d_g2s(slot + atom_bytes, &tmap_x, k0 + int32_t(kXAtom), m0, xfull_bar(st),
                             pol_x);
         };
         auto x_next = [&]() {
-            if (xw.next(p)) tile_coords_p(xw.tile, p, xmt, xnt);
+            if (xw.next(p)) xrow0 = tile_ref(xw.tile, p, gt).row0;
         };
         const uint32_t pre = n_local < S ? n_local : S;
         for (uint32_t i = 0; i < pre; ++i) {
@@ -409,14 +448,11 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
         // The first D chunks are requested before the PDL wait, so HBM keeps
         // streaming this GEMM's weights while the previous kernel drains.
         Walk<!kDecode> fw = ww;
-        uint32_t fmt, fnt;
-        tile_coords_p(fw.tile, p, fmt, fnt);
         const uint8_t* fsrc = src;
         uint32_t pf_issued = pre;  // chunks [pre, pf_issued) requested so far
         auto pf_next = [&]() {
             if (fw.next(p)) {
-                tile_coords_p(fw.tile, p, fmt, fnt);
-                fsrc = p.wimg + (uint64_t(fnt) * KB + fw.kb) * p.chunk_bytes;
+                fsrc = chunk_src(fw.tile, fw.kb);
             } else {
                 fsrc += p.chunk_bytes;
             }
@@ -581,17 +617,16 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
             i += n_iters;
             ew.kb = KB - 1;  // jump to the start of the next segment
             ew.next(p);
-            uint32_t mt, nt;
-            tile_coords_p(tile, p, mt, nt);
-            const uint32_t n = nt * kTileN + row;
-            const uint32_t m0 = mt * p.BN;
+            const TileRef tr = tile_ref(tile, p, gt);
+            const uint32_t n = tr.nt * kTileN + row;
+            const uint32_t m0 = tr.row0, mlim = tr.mlim;
             // Scales are fetched while the MMAs of this segment are in flight:
             // the token scales of the tile go to shared memory (read back as
             // broadcasts), the channel scale of this thread's row to a register.
-            const double cs = scaled ? double(p.cs[n]) : 0.0;
+            const double cs = scaled ? double(tr.cs[n]) : 0.0;
             if (scaled)
                 for (uint32_t j = et; j < p.BN; j += 128)
-                    ts_s[j] = m0 + j < p.M ? p.ts[m0 + j] : 0.f;
+                    ts_s[j] = m0 + j < mlim ? p.ts[m0 + j] : 0.f;
             // Head piece of a split tile: find the contributors and start loading
             // the first batch's chunk-0 cells now, while this segment's MMAs run.
             const bool finisher = n_iters < KB && kb0 == 0;
@@ -640,7 +675,7 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
                         int32_t a[16];
 #pragma unroll
                         for (uint32_t j = 0; j < 16; ++j) a[j] = int32_t(v[j]);
-                        store_chunk(p, m0 + ch * 16, n, a, cs, ts_s + ch * 16);
+                        store_chunk(p, m0 + ch * 16, mlim, n, a, cs, ts_s + ch * 16);
                     }
                 }
             } else if (kb0 > 0) {
@@ -738,7 +773,7 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
                         if (c + 4 >= c_end && ch + 1 < nchunks) load_batch(c_first, ch + 1);
                     }
                     if (ch == 0 && et == 0) LQG_T(10);
-                    if (n < p.N) store_chunk(p, m0 + ch * 16, n, sum, cs, ts_s + ch * 16);
+                    if (n < p.N) store_chunk(p, m0 + ch * 16, mlim, n, sum, cs, ts_s + ch * 16);
                 }
             }
             asm volatile("bar.sync 1, 128;" ::: "memory");  // ts_s reuse

@@ -416,6 +416,51 @@ class DeviceWeights:
             pass
 
 
+def _group_args(weights, xq, m_list):
+    import torch
+    if len(weights) != len(m_list) or not weights:
+        raise ValidationError("one token count per weight group is required")
+    k = weights[0].k
+    if not (xq.is_cuda and xq.dtype == torch.int8 and xq.dim() == 2 and xq.shape[1] == k
+            and xq.stride(1) == 1):
+        raise ValidationError(f"activations must be a CUDA int8 [rows, {k}] row-major tensor")
+    ms = np.ascontiguousarray(m_list, np.uint32)
+    if int(ms.sum()) != xq.shape[0]:
+        raise ValidationError("sum of group token counts must equal the activation rows")
+    handles = (C.c_void_p * len(weights))(*[w.handle for w in weights])
+    return handles, ms
+
+
+def gemm_grouped(weights, xq, ts, m_list, out=None, out_dtype=None,
+                 workspace: Workspace | None = None, stream=None):
+    """Grouped (MoE) W4A8 GEMM in one launch (lqg_gemm_w4a8_grouped): group e
+    (weights[e], m_list[e] tokens) owns the next m_list[e] rows of xq / ts /
+    out in order. Per group bit-identical to DeviceWeights.gemm."""
+    import torch
+    handles, ms = _group_args(weights, xq, m_list)
+    if out is None:
+        out = torch.empty(xq.shape[0], weights[0].n, dtype=out_dtype or torch.bfloat16,
+                          device=xq.device)
+    check(_lib.lib().lqg_gemm_w4a8_grouped(
+        handles, len(weights), xq.data_ptr(), xq.stride(0), ts.data_ptr(), ms.ctypes.data,
+        out.data_ptr(), out.stride(0), _y_code(out.dtype), workspace.handle if workspace else None,
+        _stream_ptr(stream)))
+    return out
+
+
+def gemm_grouped_accum(weights, xq, m_list, out=None, workspace: Workspace | None = None,
+                       stream=None):
+    """INT32 accumulators of the grouped GEMM."""
+    import torch
+    handles, ms = _group_args(weights, xq, m_list)
+    if out is None:
+        out = torch.empty(xq.shape[0], weights[0].n, dtype=torch.int32, device=xq.device)
+    check(_lib.lib().lqg_gemm_w4a8_grouped_accum(
+        handles, len(weights), xq.data_ptr(), xq.stride(0), ms.ctypes.data, out.data_ptr(),
+        out.stride(0), workspace.handle if workspace else None, _stream_ptr(stream)))
+    return out
+
+
 def quantize_activations(x, out_q=None, out_ts=None, check_finite: bool = False, stream=None):
     """Per-token INT8 quantization of a CUDA float32 [m, k] tensor
     (gemm.cpp:19-47, bit-exact). Returns (q int8 [m, k], ts float32 [m])."""
