@@ -119,6 +119,20 @@ int lqg_weights_from_image(const uint8_t* image, uint64_t image_bytes, const flo
 int lqg_weights_quantize(const float* d_w, int64_t ldw, uint32_t n, uint32_t k,
                          uint32_t group_size, void* stream, lqg_weights** out);
 
+/* LQWB bundle files: the reference's on-disk format (bundle.hpp:5-24,
+ * save_bundle / load_bundle, bundle.cpp:137-224), little-endian.
+ * lqg_weights_load = load_bundle + lqg_weights_create: the reference's
+ * read_bundle checks in its order and with its messages (bad magic, version,
+ * layout flag, dimensions, truncation as LQG_EIO "... (byte offset N)",
+ * trailing bytes) and then QuantizedWeightBundle::validate; plain-layout
+ * payloads are prepacked on the device.
+ * lqg_bundle_file_validate: the same checks, host only (no GPU).
+ * lqg_weights_save: the handle as a PlainRowMajor LQWB file that the
+ * reference's load_bundle reads back. */
+int lqg_weights_load(const char* path, int device, lqg_weights** out);
+int lqg_bundle_file_validate(const char* path);
+int lqg_weights_save(const lqg_weights* w, const char* path);
+
 int lqg_weights_destroy(lqg_weights* w);
 
 /* n, k, group_size of the handle. */

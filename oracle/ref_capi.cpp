@@ -11,6 +11,7 @@
 //   lq::gemm_oracle                  gemm.cpp:225-243
 //   lq::reconstruct_int8             quant.cpp:234-251
 //   lq::to_dual_mma / logical_codes  bundle.cpp:251-274, 227-249
+//   lq::save_bundle / load_bundle    bundle.cpp:213-224 (LQWB files)
 //
 // Status codes follow the reference error taxonomy (errors.hpp:15-28):
 // 0 ok, 1 ValidationError, 2 VerificationError, 3 IoError, 9 other.
@@ -97,6 +98,14 @@ int lqref_bundle_from_arrays(std::uint32_t n, std::uint32_t k, std::uint32_t g, 
         b->channel_scales.assign(cs, cs + n);
         *out = b;
     });
+}
+
+int lqref_save_bundle(const void* h, const char* path) {
+    return guarded([&] { lq::save_bundle(*static_cast<const lq::QuantizedWeightBundle*>(h), path); });
+}
+
+int lqref_load_bundle(const char* path, void** out) {
+    return guarded([&] { *out = new lq::QuantizedWeightBundle(lq::load_bundle(path)); });
 }
 
 void lqref_bundle_free(void* h) { delete static_cast<lq::QuantizedWeightBundle*>(h); }

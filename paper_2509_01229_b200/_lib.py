@@ -82,6 +82,9 @@ def lib() -> C.CDLL:
         "lqg_weights_from_image": [vp, C.c_uint64, vp, u32, u32, u32, i32, C.POINTER(vp)],
         "lqg_weights_quantize": [vp, i64, u32, u32, u32, vp, C.POINTER(vp)],
         "lqg_weights_destroy": [vp],
+        "lqg_weights_load": [C.c_char_p, i32, C.POINTER(vp)],
+        "lqg_bundle_file_validate": [C.c_char_p],
+        "lqg_weights_save": [vp, C.c_char_p],
         "lqg_weights_shape": [vp, C.POINTER(u32), C.POINTER(u32), C.POINTER(u32)],
         "lqg_weights_export": [vp, vp, vp, vp, vp],
         "lqg_workspace_create": [i32, C.POINTER(vp)],
@@ -114,6 +117,7 @@ def lib() -> C.CDLL:
 EXPORTS = [
     "lqg_bundle_validate", "lqg_image_bytes", "lqg_prepack_host", "lqg_weights_from_image",
     "lqg_weights_create", "lqg_weights_quantize", "lqg_weights_destroy",
+    "lqg_weights_load", "lqg_bundle_file_validate", "lqg_weights_save",
     "lqg_weights_shape", "lqg_weights_export", "lqg_weights_device_bytes",
     "lqg_workspace_create", "lqg_workspace_destroy", "lqg_gemm_w4a8", "lqg_gemm_w4a8_accum",
     "lqg_gemm_w4a8_grouped", "lqg_gemm_w4a8_grouped_accum",

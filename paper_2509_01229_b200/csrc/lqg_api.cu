@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <fstream>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -592,6 +593,49 @@ int lqg_weights_from_image(const uint8_t* image, uint64_t image_bytes, const flo
     return LQG_OK;
 }
 
+// Plain-layout bundles are prepacked on the device (prepack_plain_kernel):
+// the upload is the same n*k/2 + 2*n*k/g bytes as the image, and a 100+ MB
+// matrix prepacks in milliseconds instead of a host pass.
+static int create_plain_on_device(const lqg_bundle_view& b, const ImageGeom& G, int device,
+                                  lqg_weights** out) {
+    lqg_weights* w = nullptr;
+    int rc = alloc_weights(device, G, &w);
+    if (rc) return rc;
+    DeviceGuard g(device);
+    uint8_t* d_tmp = nullptr;
+    const uint64_t ng = b.n_groups;
+    const uint64_t tmp_bytes = (b.packed_bytes + 15) / 16 * 16 + 2 * ng;
+    if (cudaMalloc(&d_tmp, tmp_bytes) != cudaSuccess) {
+        lqg_weights_destroy(w);
+        return set_err(LQG_ECUDA, "prepack staging allocation failed");
+    }
+    uint8_t* d_packed = d_tmp;
+    uint8_t* d_scales = d_tmp + (b.packed_bytes + 15) / 16 * 16;
+    uint8_t* d_offsets = d_scales + ng;
+    std::vector<float> cs(uint64_t(G.NT) * kTileN, 1.0f);
+    std::memcpy(cs.data(), b.channel_scales, uint64_t(b.n) * 4);
+    cudaError_t e = cudaMemcpy(d_packed, b.packed_weights, b.packed_bytes, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(d_scales, b.group_scales, ng, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(d_offsets, b.group_offsets, ng, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(w->d_cs, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        fill_image_kernel<<<1184, 256>>>(w->d_img, uint64_t(G.NT) * G.KB, G.chunk_bytes);
+        const uint64_t threads = uint64_t(b.n) * (b.k / 32);
+        prepack_plain_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256>>>(
+            d_packed, d_scales, d_offsets, b.n, b.k, b.group_size, w->d_img, G.chunk_bytes, G.KB, G.P);
+        g_launches.fetch_add(2, std::memory_order_relaxed);
+        e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    }
+    cudaFree(d_tmp);
+    if (e != cudaSuccess) {
+        lqg_weights_destroy(w);
+        return set_err(LQG_ECUDA, std::string("device prepack failed: ") + cudaGetErrorString(e));
+    }
+    *out = w;
+    return LQG_OK;
+}
+
 int lqg_weights_create(const lqg_bundle_view* bundle, int device, lqg_weights** out) {
     if (!bundle || !out) return set_err(LQG_EVALIDATION, "null argument");
     int rc = validate_bundle(*bundle);
@@ -599,6 +643,7 @@ int lqg_weights_create(const lqg_bundle_view* bundle, int device, lqg_weights** 
     rc = device_layout_supported(bundle->group_size);
     if (rc) return rc;
     const ImageGeom G = make_geom(bundle->n, bundle->k, bundle->group_size);
+    if (bundle->layout == LQG_LAYOUT_PLAIN) return create_plain_on_device(*bundle, G, device, out);
     std::vector<uint8_t> img;
     prepack_host(*bundle, G, img);
     return lqg_weights_from_image(img.data(), img.size(), bundle->channel_scales, bundle->n,
@@ -688,6 +733,169 @@ int lqg_weights_shape(const lqg_weights* w, uint32_t* n, uint32_t* k, uint32_t* 
 
 uint64_t lqg_weights_device_bytes(const lqg_weights* w) {
     return w ? w->img_bytes + uint64_t(w->geom.NT) * kTileN * 4 : 0;
+}
+
+// ---------------------------------------------------------------- LQWB files
+// The reference's on-disk bundle format (bundle.hpp:5-24; write_bundle /
+// read_bundle, bundle.cpp:137-203), all integers little-endian. Errors carry
+// the reference's messages; stream failures are LQG_EIO with
+// "... (byte offset N)" like lq::IoError (errors.hpp:23-27).
+namespace {
+
+struct LqwbReader {
+    std::ifstream& in;
+    uint64_t off = 0;
+    int raw(void* p, uint64_t n) {
+        in.read(static_cast<char*>(p), std::streamsize(n));
+        if (uint64_t(in.gcount()) != n)
+            return set_err(LQG_EIO, "unexpected end of stream (byte offset " + std::to_string(off) + ")");
+        off += n;
+        return LQG_OK;
+    }
+    int u16(uint16_t& v) {
+        uint8_t b[2];
+        int rc = raw(b, 2);
+        v = uint16_t(b[0] | (b[1] << 8));
+        return rc;
+    }
+    int u32(uint32_t& v) {
+        uint8_t b[4];
+        int rc = raw(b, 4);
+        v = 0;
+        for (int j = 0; j < 4; ++j) v |= uint32_t(b[j]) << (8 * j);
+        return rc;
+    }
+};
+
+struct HostBundle {
+    lqg_bundle_view view{};
+    std::vector<uint8_t> packed, scales, offsets;
+    std::vector<float> cs;
+};
+
+// read_bundle (bundle.cpp:168-203) + QuantizedWeightBundle::validate.
+int read_lqwb(const char* path, HostBundle& hb) {
+    std::ifstream f(path, std::ios::binary);
+    if (!f) return set_err(LQG_EIO, std::string("cannot open ") + path + " (byte offset 0)");
+    f.seekg(0, std::ios::end);
+    const uint64_t fsize = uint64_t(f.tellg());
+    f.seekg(0, std::ios::beg);
+    LqwbReader r{f};
+    char magic[4];
+    int rc = r.raw(magic, 4);
+    if (rc) return rc;
+    if (std::memcmp(magic, "LQWB", 4) != 0) return set_err(LQG_EVALIDATION, "bad magic (not an LQWB file)");
+    uint16_t ver;
+    if ((rc = r.u16(ver))) return rc;
+    if (ver != 1) return set_err(LQG_EVALIDATION, "unsupported version " + std::to_string(ver));
+    lqg_bundle_view& b = hb.view;
+    if ((rc = r.u32(b.n)) || (rc = r.u32(b.k)) || (rc = r.u32(b.group_size))) return rc;
+    uint8_t layout;
+    if ((rc = r.raw(&layout, 1))) return rc;
+    if (layout > 1) return set_err(LQG_EVALIDATION, "unknown layout flag " + std::to_string(layout));
+    b.layout = layout;
+    b.fragment = lqg_fragment_descriptor{4, 32, 64, 32, 16, 64};
+    if (layout == LQG_LAYOUT_DUAL_MMA) {
+        auto& d = b.fragment;
+        if ((rc = r.raw(&d.warps_per_group, 1)) || (rc = r.raw(&d.threads_per_warp, 1)) ||
+            (rc = r.u16(d.mma_m)) || (rc = r.u16(d.mma_k)) ||
+            (rc = r.u16(d.elements_per_thread_per_mma)) || (rc = r.u16(d.dual_k_span)))
+            return rc;
+    }
+    if (b.n < 1 || b.k < 1) return set_err(LQG_EVALIDATION, "bundle dimensions must be >= 1");
+    if (b.group_size < 1 || b.k % b.group_size != 0)
+        return set_err(LQG_EVALIDATION, "k not divisible by group_size");
+    const uint64_t nk = uint64_t(b.n) * b.k;
+    const uint64_t ng = uint64_t(b.n) * (b.k / b.group_size);
+    // A truncated file fails at the first read that runs past its end, with
+    // that read's start offset -- decided before allocating the payload.
+    const uint64_t reads[3] = {(nk + 1) / 2, ng, ng};
+    uint64_t at = r.off;
+    for (uint64_t len : reads) {
+        if (at + len > fsize) return set_err(LQG_EIO, "unexpected end of stream (byte offset " + std::to_string(at) + ")");
+        at += len;
+    }
+    if (at + 4ull * b.n > fsize)
+        return set_err(LQG_EIO, "unexpected end of stream (byte offset " +
+                                    std::to_string(at + (fsize - at) / 4 * 4) + ")");
+    hb.packed.resize(reads[0]);
+    hb.scales.resize(ng);
+    hb.offsets.resize(ng);
+    hb.cs.resize(b.n);
+    if ((rc = r.raw(hb.packed.data(), reads[0])) || (rc = r.raw(hb.scales.data(), ng)) ||
+        (rc = r.raw(hb.offsets.data(), ng)))
+        return rc;
+    for (uint32_t i = 0; i < b.n; ++i) {
+        uint32_t bits;
+        if ((rc = r.u32(bits))) return rc;
+        std::memcpy(&hb.cs[i], &bits, 4);
+    }
+    if (r.off != fsize) return set_err(LQG_EVALIDATION, "trailing bytes after payload");
+    b.packed_weights = hb.packed.data();
+    b.packed_bytes = hb.packed.size();
+    b.group_scales = hb.scales.data();
+    b.group_offsets = hb.offsets.data();
+    b.n_groups = ng;
+    b.channel_scales = hb.cs.data();
+    return validate_bundle(b);
+}
+
+}  // namespace
+
+int lqg_bundle_file_validate(const char* path) {
+    if (!path) return set_err(LQG_EVALIDATION, "null argument");
+    HostBundle hb;
+    return read_lqwb(path, hb);
+}
+
+int lqg_weights_load(const char* path, int device, lqg_weights** out) {
+    if (!path || !out) return set_err(LQG_EVALIDATION, "null argument");
+    HostBundle hb;
+    int rc = read_lqwb(path, hb);
+    if (rc) return rc;
+    return lqg_weights_create(&hb.view, device, out);
+}
+
+// write_bundle (bundle.cpp:137-166) of the handle as a PlainRowMajor bundle.
+int lqg_weights_save(const lqg_weights* w, const char* path) {
+    if (!w || !path) return set_err(LQG_EVALIDATION, "null argument");
+    const ImageGeom& G = w->geom;
+    const uint64_t nk = uint64_t(G.n) * G.k, ng = uint64_t(G.n) * (G.k / G.g);
+    std::vector<uint8_t> packed((nk + 1) / 2, 0), scales(ng), offsets(ng);
+    std::vector<float> cs(G.n);
+    int rc = lqg_weights_export(w, packed.data(), scales.data(), offsets.data(), cs.data());
+    if (rc) return rc;
+    std::ofstream f(path, std::ios::binary);
+    if (!f) return set_err(LQG_EIO, std::string("cannot open ") + path + " for writing (byte offset 0)");
+    std::vector<uint8_t> hdr;
+    auto put = [&](uint64_t v, int nbytes) {
+        for (int i = 0; i < nbytes; ++i) hdr.push_back(uint8_t(v >> (8 * i)));
+    };
+    hdr.insert(hdr.end(), {'L', 'Q', 'W', 'B'});
+    put(1, 2);
+    put(G.n, 4);
+    put(G.k, 4);
+    put(G.g, 4);
+    put(LQG_LAYOUT_PLAIN, 1);
+    uint64_t off = 0;
+    auto wr = [&](const void* p, uint64_t n) -> int {
+        f.write(static_cast<const char*>(p), std::streamsize(n));
+        if (!f) return set_err(LQG_EIO, "write failed (byte offset " + std::to_string(off) + ")");
+        off += n;
+        return LQG_OK;
+    };
+    std::vector<uint8_t> csb(uint64_t(G.n) * 4);
+    for (uint32_t i = 0; i < G.n; ++i) {
+        uint32_t bits;
+        std::memcpy(&bits, &cs[i], 4);
+        for (int j = 0; j < 4; ++j) csb[4 * i + j] = uint8_t(bits >> (8 * j));
+    }
+    if ((rc = wr(hdr.data(), hdr.size())) || (rc = wr(packed.data(), packed.size())) ||
+        (rc = wr(scales.data(), ng)) || (rc = wr(offsets.data(), ng)) || (rc = wr(csb.data(), csb.size())))
+        return rc;
+    f.flush();
+    if (!f) return set_err(LQG_EIO, "flush failed (byte offset " + std::to_string(off) + ")");
+    return LQG_OK;
 }
 
 int lqg_weights_export(const lqg_weights* w, uint8_t* packed, uint8_t* scales, uint8_t* offsets,

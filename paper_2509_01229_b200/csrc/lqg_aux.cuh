@@ -123,6 +123,46 @@ __global__ void quantize_level2_pack_kernel(const int8_t* __restrict__ q, uint32
     }
 }
 
+// Device prepack of a plain-layout bundle (element 2j in the low nibble of
+// byte j, quant.cpp:222-228) into the image (lqg_layout.h): one thread per
+// (row, 32-element sub-block); 16 plain bytes in, one 16-byte record out with
+// the register interleave of packed.cpp:12-19 (word byte j = code j | code
+// j+4 << 4), plus the {s, a} parameter of every sub-block that starts a
+// parameter region. The image must be pre-filled (fill_image_kernel) for the
+// padding. Requires k % 32 == 0 (so every row starts on a 16-byte boundary).
+__global__ void prepack_plain_kernel(const uint8_t* __restrict__ packed, const uint8_t* __restrict__ scales,
+                                     const uint8_t* __restrict__ offsets, uint32_t n, uint32_t k,
+                                     uint32_t g, uint8_t* __restrict__ img, uint32_t chunk_bytes,
+                                     uint32_t KB, uint32_t P) {
+    const uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    const uint32_t nsub = k / 32;
+    if (t >= uint64_t(n) * nsub) return;
+    const uint32_t row = static_cast<uint32_t>(t / nsub), sb = static_cast<uint32_t>(t % nsub);
+    const uint32_t k0 = sb * 32;
+    const uint4 in = *reinterpret_cast<const uint4*>(packed + (uint64_t(row) * k + k0) / 2);
+    const uint32_t x[4] = {in.x, in.y, in.z, in.w};  // 8 codes each, plain order
+    uint32_t o[4];
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+        uint32_t word = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t lo = (x[w] >> (4 * j)) & 0xFu;       // code 8w+j
+            const uint32_t hi = (x[w] >> (4 * (j + 4))) & 0xFu; // code 8w+j+4
+            word |= (lo | (hi << 4)) << (8 * j);
+        }
+        o[w] = word;
+    }
+    const uint32_t kb = k0 / kKBlock, c = (k0 % kKBlock) / 32;
+    *reinterpret_cast<uint4*>(img + code_offset(chunk_bytes, KB, row, kb, c)) = make_uint4(o[0], o[1], o[2], o[3]);
+    const uint32_t sub_per_p = kSubBlocks / P;
+    if (c % sub_per_p == 0) {
+        const uint64_t gi = uint64_t(row) * (k / g) + k0 / g;
+        *reinterpret_cast<uint16_t*>(img + param_offset(chunk_bytes, KB, row, kb, c / sub_per_p)) =
+            uint16_t(uint32_t(scales[gi]) | (uint32_t(offsets[gi]) << 8));
+    }
+}
+
 // reconstruct_int8 through the mainloop's dequant (lqq_dequant_word): one
 // thread per (row, 32-element sub-block).
 __global__ void dequant_image_kernel(const uint8_t* __restrict__ img, uint32_t n, uint32_t k,

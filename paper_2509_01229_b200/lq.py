@@ -17,6 +17,7 @@ Differences a caller can observe:
 from __future__ import annotations
 
 import ctypes as C
+import os
 import enum
 from dataclasses import dataclass, field
 
@@ -338,6 +339,18 @@ class DeviceWeights:
         check(_lib.lib().lqg_weights_quantize(w.data_ptr(), w.stride(0), w.shape[0], w.shape[1],
                                               group_size, _stream_ptr(stream), C.byref(h)))
         return cls(h, w.device.index)
+
+    @classmethod
+    def load(cls, path: str, device: int = 0) -> "DeviceWeights":
+        """An LQWB bundle file (the reference's save_bundle format) straight to
+        the device (lqg_weights_load: load_bundle's checks, device prepack)."""
+        h = C.c_void_p()
+        check(_lib.lib().lqg_weights_load(os.fsencode(path), device, C.byref(h)))
+        return cls(h, device)
+
+    def save(self, path: str) -> None:
+        """Write this handle as a PlainRowMajor LQWB file (lqg_weights_save)."""
+        check(_lib.lib().lqg_weights_save(self.handle, os.fsencode(path)))
 
     @property
     def device_bytes(self) -> int:
