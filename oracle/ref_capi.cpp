@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "lq/bundle.hpp"
+#include "lq/cost_model.hpp"
 #include "lq/gemm.hpp"
 #include "lq/packed.hpp"
 #include "lq/quant.hpp"
@@ -97,6 +98,36 @@ int lqref_bundle_from_arrays(std::uint32_t n, std::uint32_t k, std::uint32_t g, 
         b->group_offsets.assign(offsets, offsets + ngroups);
         b->channel_scales.assign(cs, cs + n);
         *out = b;
+    });
+}
+
+// lq::load_profile + the closed-form diagnostics (cost_model.cpp:150-170).
+int lqref_profile_diag(const char* path, double* m_star, double* alpha_mem, double* alpha_comp_150) {
+    return guarded([&] {
+        const lq::HardwareProfile p = lq::load_profile(path);
+        *m_star = lq::transition_batch(p, 4, 8);
+        *alpha_mem = lq::alpha_threshold_memory(p, 4);
+        *alpha_comp_150 = lq::alpha_threshold_compute(p, 8, 150.0);
+    });
+}
+
+// lq::total_time of one W4A8 GEMM (cost_model.cpp:137-148).
+int lqref_cost_total(const char* path, std::uint64_t n, std::uint64_t k, std::uint64_t m,
+                     std::uint32_t m_t, std::uint32_t n_t, std::uint32_t k_t, double alpha,
+                     double* seconds, int* compute_bound) {
+    return guarded([&] {
+        const lq::HardwareProfile p = lq::load_profile(path);
+        lq::CostQuery q;
+        q.n = n;
+        q.k = k;
+        q.tile = lq::TileConfig{m_t, n_t, k_t};
+        q.weight_bits = 4;
+        q.act_bits = 8;
+        q.alpha = alpha;
+        q.batch = m;
+        const lq::CostBreakdown c = lq::total_time(q, p);
+        *seconds = c.total;
+        *compute_bound = c.regime == lq::Regime::ComputeBound;
     });
 }
 

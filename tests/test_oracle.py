@@ -212,3 +212,19 @@ def test_port_equals_live_reference(port, ref, n, k, g):
     if n % 64 == 0 and k % 64 == 0 and g % 64 == 0:
         codes = port.logical_codes(n, k, 0, b["packed"])
         np.testing.assert_array_equal(port.pack_dual(codes), ref.to_dual(rb).arrays()["packed"])
+
+
+def test_b200_profile_through_reference_cost_model(ref):
+    """profiles/b200.profile parses with the reference's parse_profile and puts
+    the W4A8 regime flip where the measured sweep has it (M* ~ 120,
+    cost_model.cpp:150-157); LiquidQuant's 7/8 op per element stays below the
+    memory-bound alpha threshold."""
+    import os
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
+                        "b200.profile")
+    m_star, a_mem, a_comp = ref.profile_diag(path)
+    assert 110 <= m_star <= 130
+    assert a_mem > 7 / 8 and a_comp > 7 / 8
+    t16, cb16 = ref.cost_total(path, 8192, 28672, 16, (128, 128, 256))
+    t4k, cb4k = ref.cost_total(path, 8192, 28672, 4096, (128, 128, 256))
+    assert not cb16 and cb4k
