@@ -93,13 +93,14 @@ EncodeTiledFn encode_fn() {
 
 // ---------------------------------------------------------------- workspace
 constexpr uint32_t kMaxSlots = 160;  // >= SM count of any sm_100 part
-constexpr uint64_t kSlotCells = 256ull * kTileN;  // INT32 partial-sum cells per CTA
+constexpr uint64_t kSlotCells = kSlotCellsK;  // INT32 partial-sum cells per CTA (lqg_gemm.cuh)
 
 }  // namespace
 
 struct lqg_workspace {
     int device = 0;
-    int32_t* parts = nullptr;  // [kMaxSlots][kSlotCells], INT32_MIN = not published
+    int32_t* parts = nullptr;  // [kMaxSlots][kSlotCells] split-K partials (INT32_MIN =
+                               // not published), then kMaxSlots "published" flags (0)
 };
 
 struct lqg_weights {
@@ -125,11 +126,12 @@ int workspace_create(int dev, lqg_workspace** out) {
     auto* w = new lqg_workspace();
     w->device = dev;
     DeviceGuard g(dev);
-    if (cudaMalloc(&w->parts, kMaxSlots * kSlotCells * 4) != cudaSuccess) {
+    if (cudaMalloc(&w->parts, (kMaxSlots * kSlotCells + kMaxSlots) * 4) != cudaSuccess) {
         delete w;
         return set_err(LQG_ECUDA, "workspace allocation failed");
     }
     fill_i32_kernel<<<592, 256>>>(w->parts, kMaxSlots * kSlotCells, INT32_MIN);
+    fill_i32_kernel<<<1, 256>>>(w->parts + kMaxSlots * kSlotCells, kMaxSlots, 0);
     if (cudaDeviceSynchronize() != cudaSuccess) return set_err(LQG_ECUDA, "workspace memset failed");
     *out = w;
     return LQG_OK;
@@ -398,6 +400,7 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
     p.out = d_out;
     p.ldo = ldo;
     p.parts = W->parts;
+    p.flags = reinterpret_cast<uint32_t*>(W->parts + kMaxSlots * kSlotCells);
     p.N = G.n;
     p.KB = G.KB;
     p.NT = G.NT;
@@ -420,7 +423,6 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
     p.l2_prefetch = env_u32("LQG_L2_PREFETCH_CHUNKS", decode ? 4 : 0);
     p.w_split = std::max(1u, env_u32("LQG_DEBUG_WSPLIT", 1));
     p.pdl_trigger = env_u32("LQG_PDL_TRIGGER", decode ? 2 : 0);
-    p.prewait_stages = env_u32("LQG_PREWAIT_STAGES", kMaxStages);
     p.trace_slot = static_cast<uint32_t>(g_launches.load(std::memory_order_relaxed) % 8);
     const uint32_t budget = decode ? 110 * 1024 - 3072 : 227 * 1024 - 3072;
     p.stages = std::min<uint32_t>(kMaxStages, budget / p.stage_bytes);

@@ -69,6 +69,14 @@ constexpr uint32_t kMaxStages = 16;
 constexpr uint32_t kMaxASlots = 8;
 constexpr uint32_t kACols = kKBlock / 4;   // TMEM columns per A slot (4 int8 per column)
 constexpr uint32_t kMaxBN = 256;
+// Token tiles of at most this many 16-token chunks reduce split-K partials
+// through registers with sentinel cells; larger ones via flags + TMA gather.
+constexpr uint32_t kSentinelMaxChunks = 2;
+// Split-K cells per CTA slot: the small-tile region (sentinel protocol, always
+// INT32_MIN between launches) first, then the large-tile region (flag
+// protocol, contents irrelevant between launches).
+constexpr uint32_t kSmallCells = kSentinelMaxChunks * 16 * kTileN;
+constexpr uint32_t kSlotCellsK = kSmallCells + kMaxBN * kTileN;
 
 struct TmemPlan {
     uint32_t acc_stride, acc_stages, a_base, a_slots;
@@ -91,7 +99,8 @@ struct GemmParams {
     void* out;                 // y or acc
     int64_t ldo;               // row pitch of out, in elements
     int32_t* parts;            // split-K partials: per CTA kMaxBN*128 int32 cells,
-                               // [chunk][row][16 tokens], INT32_MIN = "not published"
+                               // [chunk][quad][row] int4
+    uint32_t* flags;           // per CTA: 1 = partial published (release), reset by the finisher
     uint32_t N;                // weight rows
     uint32_t KB, NT, MT;       // k-blocks, weight tiles, token tiles (of the largest group)
     uint32_t BN;               // tokens per tile (16..256, multiple of 16)
@@ -107,7 +116,6 @@ struct GemmParams {
     uint32_t raster_gm;        // token tiles per raster group
     uint32_t trace_slot;       // LQG_TRACE builds: launch index % 8
     uint32_t pdl_trigger;
-    uint32_t prewait_stages;   // weight chunks requested before griddepcontrol.wait      // 0: after the prologue, 1: after the last load is issued, 2: after the last MMA
     uint64_t total_iters;      // tiles*KB
     uint32_t tiles;            // weight-tile x token-tile pairs (summed over groups)
 };
@@ -344,7 +352,8 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
     auto aempty_bar = [&](uint32_t a) { return bar_base + 8 * (kB + kMaxASlots + a); };
     auto accfull_bar = [&](uint32_t a) { return bar_base + 8 * (kB + 2 * kMaxASlots + a); };
     auto accempty_bar = [&](uint32_t a) { return bar_base + 8 * (kB + 2 * kMaxASlots + 2 + a); };
-    uint8_t* misc = smem + ring_bytes + 8 * (kB + 2 * kMaxASlots + 4);
+    const uint32_t fin_bar = bar_base + 8 * (kB + 2 * kMaxASlots + 4);  // split-K gather (finisher)
+    uint8_t* misc = smem + ring_bytes + 8 * (kB + 2 * kMaxASlots + 5);
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(misc);
     float* ts_s = reinterpret_cast<float*>(misc + 128);  // kMaxBN token scales
 
@@ -371,6 +380,7 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
             ptx::mbar_init(accfull_bar(a), 1);
             ptx::mbar_init(accempty_bar(a), 4);  // one arrive per epilogue warp
         }
+        ptx::mbar_init(fin_bar, 1);
         ptx::fence_mbar_init();
     }
     if (warp == 0 && lane == 0) ptx::prefetch_tmap(&tmap_x);
@@ -606,7 +616,7 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
         const uint32_t nchunks = p.BN / 16;
         const bool scaled = p.out_kind != kOutAcc;
         ptx::griddep_wait();
-        uint32_t as = 0, acc_ph = 0;
+        uint32_t as = 0, acc_ph = 0, fin_ph = 0;
         uint32_t i = 0;
         Walk<!kDecode> ew;
         ew.init(sch);
@@ -627,28 +637,30 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
             if (scaled)
                 for (uint32_t j = et; j < p.BN; j += 128)
                     ts_s[j] = m0 + j < mlim ? p.ts[m0 + j] : 0.f;
-            // Head piece of a split tile: find the contributors and start loading
-            // the first batch's chunk-0 cells now, while this segment's MMAs run.
+            // Head piece of a split tile: find its contributors now, while this
+            // segment's MMAs run; for small token tiles also request the first
+            // batch's chunk-0 cells (they are usually published by now).
             const bool finisher = n_iters < KB && kb0 == 0;
+            const bool small = nchunks <= kSentinelMaxChunks;
             uint32_t c_first = 0, c_end = 0;
             // Split-K cells of up to four contributors for one 16-token chunk:
-            // [contributor][int4]. Loaded one chunk ahead (software pipeline).
+            // [contributor][quad]. Loaded one chunk ahead (software pipeline).
             int4 cb[4][4];
-            const int32_t* parts_row = p.parts + uint64_t(row) * 16;
+            auto cell_of = [&](uint32_t c, uint32_t ch) {
+                return reinterpret_cast<int4*>(p.parts + uint64_t(c) * kSlotCellsK + (small ? 0u : kSmallCells)) +
+                       ch * 4 * kTileN + row;
+            };
             auto load_batch = [&](uint32_t c, uint32_t ch) {
                 const uint32_t nb = min(4u, c_end - c);
 #pragma unroll
                 for (uint32_t b = 0; b < 4; ++b)
-                    if (b < nb) {
-                        const int4* cell = reinterpret_cast<const int4*>(
-                            parts_row + uint64_t(c + b) * (kMaxBN * kTileN) + uint64_t(ch) * kTileN * 16);
+                    if (b < nb)
 #pragma unroll
-                        for (uint32_t q = 0; q < 4; ++q) cb[b][q] = __ldcg(cell + q);
-                    }
+                        for (uint32_t q = 0; q < 4; ++q) cb[b][q] = __ldcg(cell_of(c + b, ch) + q * kTileN);
             };
             if (finisher) {
                 split_contributors(uint64_t(tile - sch.sk_tile0), KB, G, sch.sk_total, c_first, c_end);
-                load_batch(c_first, 0);
+                if (small) load_batch(c_first, 0);
             }
             asm volatile("bar.sync 1, 128;" ::: "memory");
             ptx::mbar_wait(accfull_bar(as), acc_ph);
@@ -680,10 +692,11 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
                 }
             } else if (kb0 > 0) {
                 // Contributor piece of a split tile (always this CTA's first
-                // segment): publish the INT32 partial into this CTA's cells. No
-                // fence and no counter: |partial| <= 133120 * 127^2 < 2^31, so
-                // INT32_MIN never occurs as a value and marks "not published".
-                int32_t* slot = p.parts + uint64_t(blockIdx.x) * (kMaxBN * kTileN);
+                // segment): publish the INT32 partial into this CTA's cells.
+                // Small tiles: no fence and no flag -- |partial| <= 133120 *
+                // 127^2 < 2^31, so INT32_MIN never occurs as a value and marks
+                // "not published". Large tiles: a release flag per CTA.
+                int32_t* slot = p.parts + uint64_t(blockIdx.x) * kSlotCellsK + (small ? 0u : kSmallCells);
                 for (uint32_t ch = 0; ch < nchunks; ++ch) {
                     uint32_t v[16];
                     ptx::tmem_ld_x16(acc_taddr + ch * 16, v);
@@ -693,88 +706,145 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
                         __syncwarp();
                         if (lane == 0) ptx::mbar_arrive(accempty_bar(cur_as));
                     }
-                    int4* cell = reinterpret_cast<int4*>(slot + (ch * kTileN + row) * 16);
+                    // [chunk][quad q][row] int4 cells: a warp's stores are 512
+                    // contiguous bytes, and the finisher's bulk copy is one block
+                    int4* cell = reinterpret_cast<int4*>(slot) + ch * 4 * kTileN + row;
 #pragma unroll
                     for (uint32_t q = 0; q < 4; ++q)
-                        __stcg(cell + q, make_int4(int32_t(v[4 * q]), int32_t(v[4 * q + 1]),
-                                                   int32_t(v[4 * q + 2]), int32_t(v[4 * q + 3])));
+                        __stcg(cell + q * kTileN, make_int4(int32_t(v[4 * q]), int32_t(v[4 * q + 1]),
+                                                            int32_t(v[4 * q + 2]), int32_t(v[4 * q + 3])));
+                }
+                if (nchunks > kSentinelMaxChunks) {
+                    // large tiles: every epilogue thread's stores, then one release flag
+                    __threadfence();
+                    asm volatile("bar.sync 1, 128;" ::: "memory");
+                    if (et == 0) ptx::st_release_u32(p.flags + blockIdx.x, 1u);
                 }
                 if (et == 0) LQG_T(9);
             } else {
-                // Head piece of a split tile: this CTA finishes the tile. In
-                // stream-K order the head is the last piece processed, so the
-                // contributors' cells are normally published already: batched
-                // L2 loads (two contributors per round trip), then a spin only on
-                // cells still holding the sentinel, which are reset afterwards
-                // for the next launch. Integer addition is associative:
-                // bit-exact in any arrival order.
-                if (et == 0) LQG_TV(11, (uint64_t(c_first) << 32) | c_end);
-                for (uint32_t ch = 0; ch < nchunks; ++ch) {
-                    uint32_t v[16];
-                    ptx::tmem_ld_x16(acc_taddr + ch * 16, v);
-                    ptx::tmem_ld_wait();
-                    if (ch + 1 == nchunks) {
-                        ptx::tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) ptx::mbar_arrive(accempty_bar(cur_as));
-                    }
-                    int32_t sum[16];
+                // Head piece of a split tile: this CTA finishes the tile (in
+                // stream-K order it is the CTA's last segment). Integer addition
+                // is associative: bit-exact in any arrival order. Between
+                // launches every small-region cell holds the sentinel and every
+                // flag is 0.
+                if (small) {
+                    // Small token tiles (<= 2 chunks): the contributors' cells come
+                    // straight into registers, four contributors per L2 round
+                    // trip, the first batch requested before the accumulator wait
+                    // and the next chunk's one chunk ahead; cells still holding
+                    // the sentinel are re-read until published, then reset.
+                    for (uint32_t ch = 0; ch < nchunks; ++ch) {
+                        uint32_t v[16];
+                        ptx::tmem_ld_x16(acc_taddr + ch * 16, v);
+                        ptx::tmem_ld_wait();
+                        int32_t sum[16];
 #pragma unroll
-                    for (uint32_t j = 0; j < 16; ++j) sum[j] = int32_t(v[j]);
-                    // Contributors in batches of four: all of a batch's cells are
-                    // requested together, so the usual case (<= 4 contributors)
-                    // costs at most one L2 round trip per chunk, and the first
-                    // batch of the next chunk is requested before this chunk's
-                    // stores (software pipeline across chunks).
-                    for (uint32_t c = c_first; c < c_end; c += 4) {
-                        const uint32_t nb = min(4u, c_end - c);
-                        if (c != c_first) load_batch(c, ch);
-                        const int32_t* base = parts_row + uint64_t(c) * (kMaxBN * kTileN) + uint64_t(ch) * kTileN * 16;
-                        auto cell = [&](uint32_t b) {
-                            return reinterpret_cast<int4*>(const_cast<int32_t*>(base) + uint64_t(b) * (kMaxBN * kTileN));
-                        };
-                        // re-read, in one batch, every int4 that still holds the sentinel
-                        auto pend = [](const int4& x) {
-                            return x.x == INT32_MIN || x.y == INT32_MIN || x.z == INT32_MIN ||
-                                   x.w == INT32_MIN;
-                        };
-                        uint32_t spins = 0;
-                        for (;;) {
-                            uint32_t mask = 0;
+                        for (uint32_t j = 0; j < 16; ++j) sum[j] = int32_t(v[j]);
+                        for (uint32_t c = c_first; c < c_end; c += 4) {
+                            const uint32_t nb = min(4u, c_end - c);
+                            if (c != c_first) load_batch(c, ch);
+                            auto pend = [](const int4& x) {
+                                return x.x == INT32_MIN || x.y == INT32_MIN || x.z == INT32_MIN ||
+                                       x.w == INT32_MIN;
+                            };
+                            for (;;) {
+                                uint32_t mask = 0;
 #pragma unroll
-                            for (uint32_t b = 0; b < 4; ++b)
+                                for (uint32_t b = 0; b < 4; ++b)
 #pragma unroll
-                                for (uint32_t q = 0; q < 4; ++q)
-                                    mask |= (b < nb && pend(cb[b][q])) ? (1u << (4 * b + q)) : 0u;
-                            if (spins == 0 && et == 0 && c == c_first) LQG_T(12);
-                            if (!mask) break;
-                            ++spins;
-                            __nanosleep(32);
+                                    for (uint32_t q = 0; q < 4; ++q)
+                                        mask |= (b < nb && pend(cb[b][q])) ? (1u << (4 * b + q)) : 0u;
+                                if (!mask) break;
+                                __nanosleep(32);
 #pragma unroll
-                            for (uint32_t b = 0; b < 4; ++b)
+                                for (uint32_t b = 0; b < 4; ++b)
 #pragma unroll
-                                for (uint32_t q = 0; q < 4; ++q)
-                                    if (mask & (1u << (4 * b + q))) cb[b][q] = ptx::ld_relaxed_v4(cell(b) + q);
-                        }
-                        if (et == 0 && c == c_first) LQG_TV(13, spins);
+                                    for (uint32_t q = 0; q < 4; ++q)
+                                        if (mask & (1u << (4 * b + q)))
+                                            cb[b][q] = ptx::ld_relaxed_v4(cell_of(c + b, ch) + q * kTileN);
+                            }
 #pragma unroll
-                        for (uint32_t b = 0; b < 4; ++b) {
-                            if (b < nb) {
+                            for (uint32_t b = 0; b < 4; ++b) {
+                                if (b < nb) {
 #pragma unroll
-                                for (uint32_t q = 0; q < 4; ++q) {
-                                    sum[4 * q] += cb[b][q].x;
-                                    sum[4 * q + 1] += cb[b][q].y;
-                                    sum[4 * q + 2] += cb[b][q].z;
-                                    sum[4 * q + 3] += cb[b][q].w;
-                                    __stcg(cell(b) + q, make_int4(INT32_MIN, INT32_MIN, INT32_MIN, INT32_MIN));
+                                    for (uint32_t q = 0; q < 4; ++q) {
+                                        sum[4 * q] += cb[b][q].x;
+                                        sum[4 * q + 1] += cb[b][q].y;
+                                        sum[4 * q + 2] += cb[b][q].z;
+                                        sum[4 * q + 3] += cb[b][q].w;
+                                        __stcg(cell_of(c + b, ch) + q * kTileN,
+                                               make_int4(INT32_MIN, INT32_MIN, INT32_MIN, INT32_MIN));
+                                    }
                                 }
                             }
+                            if (c + 4 >= c_end && ch + 1 < nchunks) load_batch(c_first, ch + 1);
                         }
-                        if (c + 4 >= c_end && ch + 1 < nchunks) load_batch(c_first, ch + 1);
+                        if (n < p.N) store_chunk(p, m0 + ch * 16, mlim, n, sum, cs, ts_s + ch * 16);
                     }
-                    if (ch == 0 && et == 0) LQG_T(10);
-                    if (n < p.N) store_chunk(p, m0 + ch * 16, mlim, n, sum, cs, ts_s + ch * 16);
+                } else {
+                    // Large token tiles: this is the CTA's last segment, so the
+                    // SMEM ring is idle. Wait (acquire) until every contributor
+                    // has raised its flag, then gather the partials (one
+                    // contiguous BN*512-byte block each) by TMA bulk copies, as
+                    // many per batch as the ring holds, and sum them from SMEM:
+                    // two L2 round trips per batch instead of one per 16-token
+                    // chunk. Flags are reset for the next launch (which touches
+                    // them only after griddepcontrol.wait).
+                    const uint32_t part_bytes = p.BN * kTileN * 4;
+                    const uint32_t nb_max = max(1u, ring_bytes / part_bytes);
+                    const int4* sm4 = reinterpret_cast<const int4*>(smem);
+                    for (uint32_t c = c_first + et; c < c_end; c += 128) {
+                        while (ptx::ld_acquire_u32(p.flags + c) == 0) __nanosleep(32);
+                        p.flags[c] = 0;
+                    }
+                    asm volatile("bar.sync 1, 128;" ::: "memory");
+                    if (et == 0) LQG_T(12);
+                    for (uint32_t c0 = c_first; c0 < c_end; c0 += nb_max) {
+                        const uint32_t nb = min(nb_max, c_end - c0);
+                        const bool last_batch = c0 + nb >= c_end;
+                        if (et == 0) {
+                            ptx::fence_proxy_async();  // acquired data + prior generic SMEM reads vs TMA
+                            ptx::mbar_arrive_expect_tx(fin_bar, nb * part_bytes);
+                            for (uint32_t b = 0; b < nb; ++b)
+                                ptx::bulk_g2s(smem_base + b * part_bytes,
+                                              p.parts + uint64_t(c0 + b) * kSlotCellsK + kSmallCells, part_bytes,
+                                              fin_bar, ptx::policy_evict_first());
+                        }
+                        ptx::mbar_wait(fin_bar, fin_ph);
+                        fin_ph ^= 1;
+                        for (uint32_t ch = 0; ch < nchunks; ++ch) {
+                            uint32_t v[16];
+                            ptx::tmem_ld_x16(acc_taddr + ch * 16, v);
+                            ptx::tmem_ld_wait();
+                            int32_t sum[16];
+#pragma unroll
+                            for (uint32_t j = 0; j < 16; ++j) sum[j] = int32_t(v[j]);
+                            for (uint32_t b = 0; b < nb; ++b) {
+                                const int4* scell = sm4 + b * (part_bytes / 16) + ch * 4 * kTileN + row;
+#pragma unroll
+                                for (uint32_t q = 0; q < 4; ++q) {
+                                    const int4 x = scell[q * kTileN];
+                                    sum[4 * q] += x.x;
+                                    sum[4 * q + 1] += x.y;
+                                    sum[4 * q + 2] += x.z;
+                                    sum[4 * q + 3] += x.w;
+                                }
+                            }
+                            if (!last_batch) {
+                                // running sum back into the accumulator for the next batch
+                                ptx::tmem_st_x16(acc_taddr + ch * 16, sum);
+                            } else {
+                                if (ch == 0 && et == 0) LQG_T(10);
+                                if (n < p.N) store_chunk(p, m0 + ch * 16, mlim, n, sum, cs, ts_s + ch * 16);
+                            }
+                        }
+                        if (!last_batch) ptx::tmem_st_wait();
+                        asm volatile("bar.sync 1, 128;" ::: "memory");  // ring reads done before the next batch
+                    }
                 }
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(accempty_bar(cur_as));
             }
             asm volatile("bar.sync 1, 128;" ::: "memory");  // ts_s reuse
         }

@@ -1,2 +1,2 @@
-timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -5
-timeout 120 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
+timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+python tools/ab.py --libs variants/prev.so,paper_2509_01229_b200/liblqg.so --ms 1,16,32,64,128,256,512,1024,4096 --rounds 2 2>&1
