@@ -483,8 +483,12 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
         for (uint32_t i = pre; i < n_local; ++i) {
             ptx::mbar_wait(empty_bar(s), ph ^ 1);
             if (ptx::elect_one()) {
+#ifdef LQG_EXP_NOWTMA
+                ptx::mbar_arrive(wfull_bar(s));
+#else
                 ptx::mbar_arrive_expect_tx(wfull_bar(s), p.chunk_bytes);
                 w_copy(smem_base + s * p.stage_bytes + x_bytes, src, wfull_bar(s));
+#endif
                 x_issue(s);
                 if (pf_issued < n_local) ptx::prefetch_l2(fsrc, p.chunk_bytes);
             }
@@ -575,8 +579,15 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
 #pragma unroll
             for (uint32_t cc = 0; cc < kHalf; ++cc) {
                 const uint32_t c = wg * kHalf + cc;
+#ifdef LQG_EXP_NOLDS
+                sa[cc] = 0x8001u + c;
+                v[cc] = make_uint4(row, c, i, s);
+                (void)prm;
+                (void)wchunk;
+#else
                 sa[cc] = prm[(c >> p_shift) * kTileN + row];
                 v[cc] = *reinterpret_cast<const uint4*>(wchunk + (c * kTileN + row) * 16);
+#endif
             }
 #pragma unroll
             for (uint32_t cc = 0; cc < kHalf; ++cc) {
