@@ -410,11 +410,7 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
     p.P = G.P;
     p.chunk_bytes = G.chunk_bytes;
     p.out_kind = out_kind;
-    // Weights straight into the dequant warps' registers once every weight tile
-    // is read by several token tiles (L2-resident): the SMEM ring then carries
-    // activations only.
-    p.w_direct = env_u32("LQG_W_DIRECT", 0) && MT > 1;
-    p.stage_bytes = (BN * kKBlock + (p.w_direct ? 0u : G.chunk_bytes) + 1023) / 1024 * 1024;
+    p.stage_bytes = (BN * kKBlock + G.chunk_bytes + 1023) / 1024 * 1024;
     // Co-resident mode (opt-in, LQG_CORESIDENT=1, single group, small token
     // tiles): <= 110 KB of shared memory, 256 TMEM columns and one dequant
     // warpgroup so that two CTAs fit on an SM and the next GEMM's CTAs are
@@ -424,7 +420,7 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
     const bool decode = ng == 1 && BN <= kDecodeMaxBN && env_u32("LQG_CORESIDENT", 0);
     p.tmem_cols = decode ? 256 : 512;
     // ~24 MB of weights across the grid (enough to cover a kernel tail at HBM rate).
-    p.l2_prefetch = env_u32("LQG_L2_PREFETCH_CHUNKS", decode ? 4 : (p.w_direct ? 6 : 0));
+    p.l2_prefetch = env_u32("LQG_L2_PREFETCH_CHUNKS", decode ? 4 : 0);
     p.w_split = std::max(1u, env_u32("LQG_DEBUG_WSPLIT", 1));
     p.pdl_trigger = env_u32("LQG_PDL_TRIGGER", decode ? 2 : 0);
     p.trace_slot = static_cast<uint32_t>(g_launches.load(std::memory_order_relaxed) % 8);
