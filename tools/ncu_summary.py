@@ -118,18 +118,50 @@ def launches(path):
     return "\n".join(lines)
 
 
+def traffic(paths):
+    """profiles/ncu_summary.json for bench.py: DRAM bytes (read + write) and
+    device time per launch of each LLaMA-2-70B layer GEMM at M = 16 and 4096
+    (reports named prof_<n>x<k>_m<M>.ncu-rep), summed per 4-GEMM group like the
+    bench's roofline entries."""
+    import os
+    import re
+    out = {"shapes": {}, "how": "ncu --set full --clock-control none, one launch per shape "
+                                "(tools/profile_one.py, 3rd launch), dram__bytes_read.sum + "
+                                "dram__bytes_write.sum"}
+    for path in paths:
+        m = re.search(r"prof_(\d+)x(\d+)_m(\d+)", os.path.basename(path))
+        if not m:
+            continue
+        n, k, mm = map(int, m.groups())
+        r = rep(path)[0]
+        out["shapes"][f"{n}x{k}_m{mm}"] = {"traffic_bytes": r.get("traffic_bytes"),
+                                           "duration_s": r.get("duration_s"),
+                                           "tensor_active_pct": r.get(
+                                               "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"),
+                                           "dram_pct": r.get(
+                                               "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed")}
+    for mm in (16, 4096):
+        vals = [v["traffic_bytes"] for kk, v in out["shapes"].items() if kk.endswith(f"_m{mm}")]
+        if vals and all(v is not None for v in vals):
+            out[f"traffic_bytes_M{mm}"] = sum(vals)
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("mode", choices=["rep", "launches"])
-    ap.add_argument("path")
+    ap.add_argument("mode", choices=["rep", "launches", "traffic"])
+    ap.add_argument("path", nargs="+")
     ap.add_argument("--bytes", type=float)
     ap.add_argument("--ops", type=float)
     a = ap.parse_args()
     if a.mode == "rep":
-        json.dump(rep(a.path, a.bytes, a.ops), sys.stdout, indent=1)
+        json.dump(rep(a.path[0], a.bytes, a.ops), sys.stdout, indent=1)
+        print()
+    elif a.mode == "traffic":
+        json.dump(traffic(a.path), sys.stdout, indent=1)
         print()
     else:
-        print(launches(a.path))
+        print(launches(a.path[0]))
 
 
 if __name__ == "__main__":
