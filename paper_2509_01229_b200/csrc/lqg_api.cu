@@ -118,6 +118,9 @@ struct lqg_weights {
     size_t ts_cap = 0;
     void* d_y = nullptr;
     size_t y_cap = 0;
+    // host-call pipeline: copy-in / copy-out streams and per-chunk events
+    cudaStream_t s_in = nullptr, s_out = nullptr;
+    cudaEvent_t ev[2 * 8 + 1] = {};
 };
 
 namespace {
@@ -720,6 +723,10 @@ int lqg_weights_destroy(lqg_weights* w) {
     cudaFree(w->d_x);
     cudaFree(w->d_ts);
     cudaFree(w->d_y);
+    if (w->s_in) cudaStreamDestroy(w->s_in);
+    if (w->s_out) cudaStreamDestroy(w->s_out);
+    for (cudaEvent_t e : w->ev)
+        if (e) cudaEventDestroy(e);
     lqg_workspace_destroy(w->ws);
     delete w;
     return LQG_OK;
@@ -1003,17 +1010,52 @@ static int host_call(const lqg_weights* wc, const int8_t* x, const float* ts, ui
     if (!rc) rc = ensure_cap(reinterpret_cast<void**>(&w->d_ts), &w->ts_cap, size_t(m) * 4);
     if (!rc) rc = ensure_cap(&w->d_y, &w->y_cap, size_t(m) * G.n * ebytes);
     if (rc) return rc;
-    if (ldx == int64_t(G.k)) {
-        LQG_CUDA(cudaMemcpyAsync(w->d_x, x, size_t(m) * G.k, cudaMemcpyHostToDevice, st));
-    } else {
-        LQG_CUDA(cudaMemcpy2DAsync(w->d_x, ldx, x, G.k, G.k, m, cudaMemcpyHostToDevice, st));
+    // Large calls are cut into row chunks pipelined over three streams:
+    // H2D of chunk c+1 and D2H of chunk c-1 (PCIe is full duplex) overlap the
+    // GEMM of chunk c, so the call costs ~max(H2D, D2H) instead of their sum
+    // plus the GEMM. Small calls (latency-bound) stay one chunk.
+    const uint32_t per = m >= 2048 ? std::max<uint32_t>(1024, (m + 7) / 8) : m;
+    const uint32_t nchunk = (m + per - 1) / per;
+    if (nchunk > 1 && !w->s_in) {
+        LQG_CUDA(cudaStreamCreateWithFlags(&w->s_in, cudaStreamNonBlocking));
+        LQG_CUDA(cudaStreamCreateWithFlags(&w->s_out, cudaStreamNonBlocking));
+        for (cudaEvent_t& e : w->ev) LQG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
-    if (kind != kOutAcc)
-        LQG_CUDA(cudaMemcpyAsync(w->d_ts, ts, size_t(m) * 4, cudaMemcpyHostToDevice, st));
-    rc = launch_gemm(w, w->d_x, ldx, w->d_ts, m, w->d_y, G.n, kind, nullptr, st);
-    if (rc) return rc;
-    LQG_CUDA(cudaMemcpyAsync(y, w->d_y, size_t(m) * G.n * ebytes, cudaMemcpyDeviceToHost, st));
-    LQG_CUDA(cudaStreamSynchronize(st));
+    cudaStream_t s_in = nchunk > 1 ? w->s_in : st, s_out = nchunk > 1 ? w->s_out : st;
+    if (nchunk > 1) {  // the copies start after the caller's prior work on st
+        LQG_CUDA(cudaEventRecord(w->ev[16], st));
+        LQG_CUDA(cudaStreamWaitEvent(s_in, w->ev[16], 0));
+        LQG_CUDA(cudaStreamWaitEvent(s_out, w->ev[16], 0));
+    }
+    const size_t yrow = size_t(G.n) * ebytes;
+    for (uint32_t c = 0; c < nchunk; ++c) {
+        const uint32_t r0 = c * per, rows = std::min(per, m - r0);
+        int8_t* dx = w->d_x + size_t(r0) * ldx;
+        if (ldx == int64_t(G.k)) {
+            LQG_CUDA(cudaMemcpyAsync(dx, x + size_t(r0) * G.k, size_t(rows) * G.k, cudaMemcpyHostToDevice, s_in));
+        } else {
+            LQG_CUDA(cudaMemcpy2DAsync(dx, ldx, x + size_t(r0) * G.k, G.k, G.k, rows,
+                                       cudaMemcpyHostToDevice, s_in));
+        }
+        if (kind != kOutAcc)
+            LQG_CUDA(cudaMemcpyAsync(w->d_ts + r0, ts + r0, size_t(rows) * 4, cudaMemcpyHostToDevice, s_in));
+        if (nchunk > 1) {
+            LQG_CUDA(cudaEventRecord(w->ev[2 * (c % 8)], s_in));
+            LQG_CUDA(cudaStreamWaitEvent(st, w->ev[2 * (c % 8)], 0));
+        }
+        rc = launch_gemm(w, dx, ldx, w->d_ts + r0, rows, static_cast<uint8_t*>(w->d_y) + r0 * yrow, G.n,
+                         kind, nullptr, st);
+        if (rc) return rc;
+        if (nchunk > 1) {
+            LQG_CUDA(cudaEventRecord(w->ev[2 * (c % 8) + 1], st));
+            LQG_CUDA(cudaStreamWaitEvent(s_out, w->ev[2 * (c % 8) + 1], 0));
+        }
+        LQG_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(y) + r0 * yrow,
+                                 static_cast<uint8_t*>(w->d_y) + r0 * yrow, rows * yrow,
+                                 cudaMemcpyDeviceToHost, s_out));
+    }
+    LQG_CUDA(cudaStreamSynchronize(s_out));
+    if (nchunk > 1) LQG_CUDA(cudaStreamSynchronize(st));
     return LQG_OK;
 }
 

@@ -338,3 +338,27 @@ def test_reference_acceptance_gate_through_cpp_dropin(torch_cuda):
     r = subprocess.run([binary, "--criterion", "6"], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "[PASS] criterion 6" in r.stdout, r.stdout
+
+
+@pytest.mark.parametrize("m", [2048, 3001, 9000])
+def test_host_call_pipelined_chunks(torch_cuda, lqg, m):
+    """lqg_gemm_w4a8_host cuts large calls into row chunks pipelined over
+    copy-in / GEMM / copy-out streams; the result must equal the single device
+    launch byte for byte (pinned and pageable host buffers, accumulators too)."""
+    torch = torch_cuda
+    g = torch.Generator(device="cuda").manual_seed(m)
+    n, k = 384, 640
+    dw = lqg.DeviceWeights.quantize(torch.randn(n, k, generator=g, device="cuda") * 0.02, 128)
+    q, ts = lqg.quantize_activations(torch.randn(m, k, generator=g, device="cuda"))
+    y_dev = dw.gemm(q, ts).cpu()
+    for pin in (True, False):
+        qh, th = q.cpu(), ts.cpu()
+        yh = torch.empty(m, n, dtype=torch.bfloat16)
+        if pin:
+            qh, th, yh = qh.pin_memory(), th.pin_memory(), yh.pin_memory()
+        dw.gemm_host(qh, th, yh)
+        assert torch.equal(yh, y_dev)
+    acc_h = np.zeros((m, n), np.int32)
+    lqg._lib.lib().lqg_gemm_w4a8_accum_host(dw.handle, q.cpu().numpy().ctypes.data, m,
+                                            acc_h.ctypes.data, None)
+    np.testing.assert_array_equal(acc_h, dw.gemm_accum(q).cpu().numpy())
