@@ -165,6 +165,19 @@ int lqg_gemm_w4a8(const lqg_weights* w, const int8_t* d_x, int64_t ldx,
                   const float* d_token_scales, uint32_t m, void* d_y, int64_t ldy, int y_dtype,
                   lqg_workspace* ws, void* stream);
 
+/* lqg_gemm_w4a8 whose epilogue stores every output tile into n_ys (1..8)
+ * destinations with the same pitch: d_ys[0] plus up to 7 more, typically
+ * the peers' Y buffers mapped over NVLink (CUDA IPC / symmetric memory). In
+ * the N-split driver each rank passes its column slice of every rank's full
+ * Y (base + column offset, ldy = n_full), so the row-output all-gather
+ * happens inside the GEMM epilogue, tile by tile, overlapped with the
+ * mainloop; the caller then only needs a cross-GPU barrier. Values are
+ * bit-identical to lqg_gemm_w4a8. */
+int lqg_gemm_w4a8_fanout(const lqg_weights* w, const int8_t* d_x, int64_t ldx,
+                         const float* d_token_scales, uint32_t m, void* const* d_ys,
+                         uint32_t n_ys, int64_t ldy, int y_dtype, lqg_workspace* ws,
+                         void* stream);
+
 /* INT32 accumulators only (gemm.cpp:138-211), bit-exact. d_acc: m x ldacc. */
 int lqg_gemm_w4a8_accum(const lqg_weights* w, const int8_t* d_x, int64_t ldx, uint32_t m,
                         int32_t* d_acc, int64_t ldacc, lqg_workspace* ws, void* stream);

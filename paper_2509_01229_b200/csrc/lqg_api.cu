@@ -337,7 +337,8 @@ constexpr uint32_t kMaxGroups = 64;  // experts per grouped launch
 // and Y, concatenated in group order.
 int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* m_list,
                 const int8_t* d_x, int64_t ldx, const float* d_ts, void* d_out, int64_t ldo,
-                uint32_t out_kind, lqg_workspace* ws, cudaStream_t stream) {
+                uint32_t out_kind, lqg_workspace* ws, cudaStream_t stream,
+                void* const* fan = nullptr, uint32_t n_fan = 0) {
     const lqg_weights* w = ws_list[0];
     const ImageGeom& G = w->geom;
     uint64_t rows = 0;
@@ -402,6 +403,12 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
     p.ts = d_ts;
     p.out = d_out;
     p.ldo = ldo;
+    if (n_fan > 7) return set_err(LQG_EVALIDATION, "at most 8 output destinations");
+    for (uint32_t r = 0; r < n_fan; ++r) {
+        if (!fan[r]) return set_err(LQG_EVALIDATION, "null device pointer");
+        p.fan[r] = fan[r];
+    }
+    p.n_fan = n_fan;
     p.parts = W->parts;
     p.flags = reinterpret_cast<uint32_t*>(W->parts + kMaxSlots * kSlotCells);
     p.N = G.n;
@@ -420,7 +427,7 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
     // resident while this one drains. Measured on B200 it loses to one CTA per
     // SM with the full 227 KB ring (LLaMA-2-70B 4-layer step at M = 16: 95 vs
     // 81 us): the halved ring slows the mainloop more than the earlier start gains.
-    const bool decode = ng == 1 && BN <= kDecodeMaxBN && env_u32("LQG_CORESIDENT", 0);
+    const bool decode = ng == 1 && n_fan == 0 && BN <= kDecodeMaxBN && env_u32("LQG_CORESIDENT", 0);
     p.tmem_cols = decode ? 256 : 512;
     // ~24 MB of weights across the grid (enough to cover a kernel tail at HBM rate).
     p.l2_prefetch = env_u32("LQG_L2_PREFETCH_CHUNKS", decode ? 4 : 0);
@@ -461,13 +468,16 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
     DeviceGuard dg(w->device);
     cudaError_t e = cudaSuccess;
     std::call_once(g_attr_once[w->device % 64], [&] {
-        e = cudaFuncSetAttribute(lqg_w4a8_gemm_kernel<true, 1>,
+        e = cudaFuncSetAttribute(lqg_w4a8_gemm_kernel<true, 1, false>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(lqg_w4a8_gemm_kernel<false, 1>,
+            e = cudaFuncSetAttribute(lqg_w4a8_gemm_kernel<false, 1, false>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(lqg_w4a8_gemm_kernel<false, kMaxGroups>,
+            e = cudaFuncSetAttribute(lqg_w4a8_gemm_kernel<false, 1, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(lqg_w4a8_gemm_kernel<false, kMaxGroups, false>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     });
     if (e != cudaSuccess) return set_err(LQG_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
@@ -482,15 +492,17 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     if (ng > 1) {
-        LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<false, kMaxGroups>, tmap, p, gt));
+        LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<false, kMaxGroups, false>, tmap, p, gt));
     } else {
         GroupTable<1> g1{};
         g1.e[0] = gt.e[0];
         g1.n = 1;
-        if (decode)
-            LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<true, 1>, tmap, p, g1));
+        if (n_fan)
+            LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<false, 1, true>, tmap, p, g1));
+        else if (decode)
+            LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<true, 1, false>, tmap, p, g1));
         else
-            LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<false, 1>, tmap, p, g1));
+            LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<false, 1, false>, tmap, p, g1));
     }
     g_launches.fetch_add(1, std::memory_order_relaxed);
     LQG_CUDA(cudaGetLastError());
@@ -988,6 +1000,19 @@ int lqg_gemm_w4a8_grouped_accum(const lqg_weights* const* weights, uint32_t num_
         return set_err(LQG_EVALIDATION, "num_groups must be in [1, " + std::to_string(kMaxGroups) + "]");
     return launch_core(weights, num_groups, m, d_x, ldx, nullptr, d_acc, ldacc, kOutAcc, ws,
                        static_cast<cudaStream_t>(stream));
+}
+
+int lqg_gemm_w4a8_fanout(const lqg_weights* w, const int8_t* d_x, int64_t ldx,
+                         const float* d_token_scales, uint32_t m, void* const* d_ys, uint32_t n_ys,
+                         int64_t ldy, int y_dtype, lqg_workspace* ws, void* stream) {
+    if (!w || !d_ys) return set_err(LQG_EVALIDATION, "null argument");
+    if (n_ys < 1 || n_ys > 8) return set_err(LQG_EVALIDATION, "n_ys must be in [1, 8]");
+    if (m < 1) return set_err(LQG_EVALIDATION, "activation dimensions must be >= 1");
+    uint32_t kind;
+    int rc = out_kind_of(y_dtype, &kind);
+    if (rc) return rc;
+    return launch_core(&w, 1, &m, d_x, ldx, d_token_scales, d_ys[0], ldy, kind, ws,
+                       static_cast<cudaStream_t>(stream), d_ys + 1, n_ys - 1);
 }
 
 int lqg_gemm_w4a8_accum(const lqg_weights* w, const int8_t* d_x, int64_t ldx, uint32_t m, int32_t* d_acc,

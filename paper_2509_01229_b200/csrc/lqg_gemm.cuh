@@ -97,7 +97,9 @@ __host__ __device__ inline TmemPlan tmem_plan(uint32_t BN, uint32_t cols) {
 struct GemmParams {
     const float* ts;           // token scales (all rows)
     void* out;                 // y or acc
-    int64_t ldo;               // row pitch of out, in elements
+    int64_t ldo;               // row pitch of out (and of every fan-out copy), in elements
+    void* fan[7];              // extra destinations receiving the same tile (e.g. peer GPUs'
+    uint32_t n_fan;            //   Y over NVLink: the fused all-gather of the N-split driver)
     int32_t* parts;            // split-K partials: per CTA kMaxBN*128 int32 cells,
                                // [chunk][quad][row] int4
     uint32_t* flags;           // per CTA: 1 = partial published (release), reset by the finisher
@@ -279,36 +281,44 @@ __device__ __forceinline__ TileRef tile_ref(uint32_t t, const GemmParams& p, con
 // to right, then the requested cast (RNE). cs_d is double(cs). One call stores
 // the 16 tokens [m0, m0+16) of output column n; the output kind is a template
 // parameter so every store loop is branch-free (dispatch once per chunk).
-template <uint32_t kKind>
+template <uint32_t kKind, bool kFan>
 __device__ __forceinline__ void store_chunk_k(const GemmParams& p, uint32_t m0, uint32_t mlim,
                                               uint32_t n, const int32_t (&acc)[16], double cs_d,
                                               const float* ts) {
     const uint32_t mend = min(16u, mlim > m0 ? mlim - m0 : 0u);
     uint64_t idx = uint64_t(m0) * uint64_t(p.ldo) + n;
+    // one element to the primary output and every fan-out destination
+    auto put = [&](uint64_t i, auto v) {
+        using T = decltype(v);
+        static_cast<T*>(p.out)[i] = v;
+        if (kFan)
+            for (uint32_t r = 0; r < p.n_fan; ++r) static_cast<T*>(p.fan[r])[i] = v;
+    };
 #pragma unroll
     for (uint32_t j = 0; j < 16; ++j, idx += p.ldo) {
         if (j >= mend) break;
         if (kKind == kOutAcc) {
-            static_cast<int32_t*>(p.out)[idx] = acc[j];
+            put(idx, acc[j]);
         } else {
             const float y = __double2float_rn(__dmul_rn(__dmul_rn(double(acc[j]), cs_d), double(ts[j])));
             if (kKind == kOutF32)
-                static_cast<float*>(p.out)[idx] = y;
+                put(idx, y);
             else if (kKind == kOutF16)
-                static_cast<__half*>(p.out)[idx] = __float2half_rn(y);
+                put(idx, __float2half_rn(y));
             else
-                static_cast<__nv_bfloat16*>(p.out)[idx] = __float2bfloat16_rn(y);
+                put(idx, __float2bfloat16_rn(y));
         }
     }
 }
 
+template <bool kFan>
 __device__ __forceinline__ void store_chunk(const GemmParams& p, uint32_t m0, uint32_t mlim, uint32_t n,
                                             const int32_t (&acc)[16], double cs_d, const float* ts) {
     switch (p.out_kind) {
-        case kOutAcc: store_chunk_k<kOutAcc>(p, m0, mlim, n, acc, cs_d, ts); break;
-        case kOutF32: store_chunk_k<kOutF32>(p, m0, mlim, n, acc, cs_d, ts); break;
-        case kOutF16: store_chunk_k<kOutF16>(p, m0, mlim, n, acc, cs_d, ts); break;
-        default: store_chunk_k<kOutBF16>(p, m0, mlim, n, acc, cs_d, ts); break;
+        case kOutAcc: store_chunk_k<kOutAcc, kFan>(p, m0, mlim, n, acc, cs_d, ts); break;
+        case kOutF32: store_chunk_k<kOutF32, kFan>(p, m0, mlim, n, acc, cs_d, ts); break;
+        case kOutF16: store_chunk_k<kOutF16, kFan>(p, m0, mlim, n, acc, cs_d, ts); break;
+        default: store_chunk_k<kOutBF16, kFan>(p, m0, mlim, n, acc, cs_d, ts); break;
     }
 }
 
@@ -329,7 +339,10 @@ __device__ __forceinline__ void trace(uint32_t slot, uint32_t e) {
 // kDecode: two CTAs per SM (<= 110 KB SMEM, 256 TMEM columns, <= 72 registers)
 // so consecutive GEMMs overlap under PDL; otherwise one CTA per SM.
 // kG > 1: grouped launch over up to kG weight groups (MoE experts).
-template <bool kDecode, uint32_t kG>
+// kFan: the epilogue also stores every tile into p.fan[0..n_fan) (fused
+// all-gather of the N-split driver); a separate instantiation so the plain
+// kernel's epilogue is untouched.
+template <bool kDecode, uint32_t kG, bool kFan>
 __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
     lqg_w4a8_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const GemmParams p,
                          const __grid_constant__ GroupTable<kG> gt) {
@@ -698,7 +711,7 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
                         int32_t a[16];
 #pragma unroll
                         for (uint32_t j = 0; j < 16; ++j) a[j] = int32_t(v[j]);
-                        store_chunk(p, m0 + ch * 16, mlim, n, a, cs, ts_s + ch * 16);
+                        store_chunk<kFan>(p, m0 + ch * 16, mlim, n, a, cs, ts_s + ch * 16);
                     }
                 }
             } else if (kb0 > 0) {
@@ -790,7 +803,7 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
                             }
                             if (c + 4 >= c_end && ch + 1 < nchunks) load_batch(c_first, ch + 1);
                         }
-                        if (n < p.N) store_chunk(p, m0 + ch * 16, mlim, n, sum, cs, ts_s + ch * 16);
+                        if (n < p.N) store_chunk<kFan>(p, m0 + ch * 16, mlim, n, sum, cs, ts_s + ch * 16);
                     }
                 } else {
                     // Large token tiles: this is the CTA's last segment, so the
@@ -846,7 +859,7 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
                                 ptx::tmem_st_x16(acc_taddr + ch * 16, sum);
                             } else {
                                 if (ch == 0 && et == 0) LQG_T(10);
-                                if (n < p.N) store_chunk(p, m0 + ch * 16, mlim, n, sum, cs, ts_s + ch * 16);
+                                if (n < p.N) store_chunk<kFan>(p, m0 + ch * 16, mlim, n, sum, cs, ts_s + ch * 16);
                             }
                         }
                         if (!last_batch) ptx::tmem_st_wait();

@@ -376,6 +376,25 @@ class DeviceWeights:
             _stream_ptr(stream)))
         return out
 
+    def gemm_fanout(self, xq, ts, outs, workspace: Workspace | None = None, stream=None):
+        """Y written by the epilogue into every tensor of `outs` (same shape and
+        row pitch; local or peer-mapped device memory): lqg_gemm_w4a8_fanout.
+        Each `out` may be a column slice of a wider row-major buffer."""
+        self._check_x(xq)
+        m = xq.shape[0]
+        if not 1 <= len(outs) <= 8:
+            raise ValidationError("1..8 output tensors")
+        ld = outs[0].stride(0)
+        for o in outs:
+            if o.shape[0] < m or o.shape[1] != self.n or o.stride(0) != ld or o.stride(1) != 1 \
+                    or o.dtype != outs[0].dtype:
+                raise ValidationError("fan-out outputs must share shape, dtype and row pitch")
+        ptrs = (C.c_void_p * len(outs))(*[o.data_ptr() for o in outs])
+        check(_lib.lib().lqg_gemm_w4a8_fanout(
+            self.handle, xq.data_ptr(), xq.stride(0), ts.data_ptr(), m, ptrs, len(outs), ld,
+            _y_code(outs[0].dtype), workspace.handle if workspace else None, _stream_ptr(stream)))
+        return outs[0]
+
     def gemm_accum(self, xq, out=None, workspace: Workspace | None = None, stream=None):
         import torch
         self._check_x(xq)

@@ -10,6 +10,15 @@ Y equals the single-GPU Y byte for byte.
 Rank r owns weight rows [start_r, end_r), 128-row aligned (one tcgen05 M tile)
 so every shard is a whole number of device tiles; shards are padded to the
 largest one for the fixed-size all-gather.
+
+Two gather modes:
+  * "nccl" (default): the kernel writes Y_r, then one NCCL all_gather_into_tensor
+    over NVLink plus a strided copy (`gather_columns`).
+  * "p2p": the row output lives in NVLink symmetric memory
+    (torch.distributed._symmetric_memory); every rank's GEMM epilogue stores
+    its column slice straight into every rank's Y (lqg_gemm_w4a8_fanout), so
+    the all-gather is fused into the GEMM tile by tile and only a cross-GPU
+    barrier remains.
 """
 from __future__ import annotations
 
@@ -114,12 +123,16 @@ class ColumnParallelW4A8:
     """
 
     def __init__(self, n: int, k: int, group_size: int, rank: int, world: int, group=None,
-                 local_gemm: Callable | None = None, device_weights=None):
+                 local_gemm: Callable | None = None, device_weights=None, gather: str = "nccl"):
+        if gather not in ("nccl", "p2p"):
+            raise ValidationError("gather must be 'nccl' or 'p2p'")
         self.n, self.k, self.group_size = n, k, group_size
         self.plan = ShardPlan(n, world, rank, shard_rows(n, world))
         self.group = group
         self.dw = device_weights
         self._local = local_gemm
+        self.gather = gather
+        self._symm = None  # (max_m, dtype, local Y, peer Ys, handle)
 
     @classmethod
     def from_bundle(cls, b: QuantizedWeightBundle, rank: int, world: int, group=None,
@@ -148,8 +161,44 @@ class ColumnParallelW4A8:
             return self._local(xq, ts)
         return self.dw.gemm(xq, ts, out=out)
 
-    def forward(self, xq, ts, out=None, y_local=None):
+    def _symmetric_output(self, m: int, dtype, device):
+        """Y [max_m, n] in symmetric memory on every rank + the peers' views."""
+        import torch
+        import torch.distributed as dist
+        if self._symm is not None and self._symm[0] >= m and self._symm[1] == dtype:
+            return self._symm
+        import torch.distributed._symmetric_memory as symm_mem
+        max_m = max(m, self._symm[0] if self._symm else 0)
+        y = symm_mem.empty(max_m, self.n, dtype=dtype, device=device)
+        world = self.plan.world
+        if world > 1:
+            group = self.group if self.group is not None else dist.group.WORLD
+            hdl = symm_mem.rendezvous(y, group)
+            peers = [y if r == self.plan.rank else hdl.get_buffer(r, [max_m, self.n], dtype)
+                     for r in range(world)]
+        else:
+            hdl, peers = None, [y]
+        self._symm = (max_m, dtype, y, peers, hdl)
+        return self._symm
+
+    def forward(self, xq, ts, out=None, y_local=None, out_dtype=None):
         """Y [m, n] = gather_r( X W_r^T * cs_r * ts )."""
+        if self.gather == "p2p" and self._local is None:
+            import torch
+            m = xq.shape[0]
+            dtype = out_dtype or (out.dtype if out is not None else torch.bfloat16)
+            _, _, y, peers, hdl = self._symmetric_output(m, dtype, xq.device)
+            s, e = self.plan.rows
+            # this rank's column slice of every rank's Y (itself first)
+            me = self.plan.rank
+            order = [me] + [r for r in range(self.plan.world) if r != me]
+            self.dw.gemm_fanout(xq, ts, [peers[r][:m, s:e] for r in order])
+            if hdl is not None:
+                hdl.barrier()  # every rank's slices have landed in every Y
+            if out is not None:
+                out.copy_(y[:m])
+                return out
+            return y[:m]
         y_r = self.local(xq, ts, out=y_local)
         return gather_columns(y_r, self.plan, self.group, out=out)
 

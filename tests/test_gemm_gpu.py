@@ -362,3 +362,42 @@ def test_host_call_pipelined_chunks(torch_cuda, lqg, m):
     lqg._lib.lib().lqg_gemm_w4a8_accum_host(dw.handle, q.cpu().numpy().ctypes.data, m,
                                             acc_h.ctypes.data, None)
     np.testing.assert_array_equal(acc_h, dw.gemm_accum(q).cpu().numpy())
+
+
+def test_fanout_epilogue_writes_every_destination(torch_cuda, lqg):
+    """lqg_gemm_w4a8_fanout (the fused all-gather building block of the N-split
+    driver): every destination -- here column slices of several full-width
+    buffers on this GPU, standing in for the peers' Y over NVLink -- receives
+    exactly the lqg_gemm_w4a8 output; columns outside the slice stay untouched."""
+    torch = torch_cuda
+    g = torch.Generator(device="cuda").manual_seed(5)
+    n_full, k, m = 1024, 768, 300
+    s, e = 256, 640
+    dw = lqg.DeviceWeights.quantize(torch.randn(e - s, k, generator=g, device="cuda") * 0.02, 128)
+    q, ts = lqg.quantize_activations(torch.randn(m, k, generator=g, device="cuda"))
+    ref = dw.gemm(q, ts)
+    bufs = [torch.full((m, n_full), 7.0, dtype=torch.bfloat16, device="cuda") for _ in range(4)]
+    dw.gemm_fanout(q, ts, [b[:, s:e] for b in bufs])
+    for b in bufs:
+        assert torch.equal(b[:, s:e], ref)
+        assert bool((b[:, :s] == 7).all()) and bool((b[:, e:] == 7).all())
+    with pytest.raises(lqg.ValidationError):
+        dw.gemm_fanout(q, ts, [bufs[0][:, s:e], bufs[1][:, s:e - 1]])
+
+
+def test_column_parallel_p2p_single_rank(torch_cuda, lqg):
+    """tp.ColumnParallelW4A8(gather='p2p') on one rank: symmetric-memory output
+    written by the fan-out epilogue equals the plain GEMM."""
+    torch = torch_cuda
+    from paper_2509_01229_b200 import tp
+    g = torch.Generator(device="cuda").manual_seed(6)
+    n, k, m = 512, 1024, 40
+    w = torch.randn(n, k, generator=g, device="cuda") * 0.02
+    q, ts = lqg.quantize_activations(torch.randn(m, k, generator=g, device="cuda"))
+    layer = tp.ColumnParallelW4A8.from_weights(w, 128, 0, 1)
+    layer.gather = "p2p"
+    try:
+        y = layer(q, ts)
+    except Exception as exc:  # symmetric memory needs a distributed backend on some builds
+        pytest.skip(f"symmetric memory unavailable: {exc}")
+    assert torch.equal(y, layer.dw.gemm(q, ts))

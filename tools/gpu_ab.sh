@@ -1,2 +1,2 @@
-timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
-timeout 900 python bench.py --no-cpu-baseline --no-sweep 2>/dev/null | python -c "import json,sys; d=json.loads([l for l in sys.stdin if l.startswith('{')][-1]); print(d['value'], d['e2e'])"
+timeout 600 python -m pytest tests -m gpu -x -q -rs 2>&1 | tail -5
+python tools/ab.py --libs variants/prev2.so,paper_2509_01229_b200/liblqg.so --ms 1,16,256,4096 --rounds 2 2>&1
