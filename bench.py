@@ -426,6 +426,12 @@ def run_lqg(args, workload):
                            "unit": "GB/s", "frac": small["hbm_gbs"] / peaks["hbm_gbs"],
                            "traffic": prof.get("traffic_bytes_M16"),
                            "at": "M=16, 4 layer GEMMs, algorithmic bytes", "peak_src": peaks["hbm_src"]}
+    moe = None
+    if world == 1 and not args.no_sweep:
+        try:
+            moe = run_moe(lqg, dev, peaks)
+        except Exception as exc:  # extra evidence must never sink the main number
+            moe = {"error": repr(exc)[:200]}
     line = {
         "metric": "W4A8 GEMM TOPS (llama2-70b layer shapes, M sweep 1..4096)",
         "value": value, "unit": "TOPS", "n_gpus": world, "steps": args.steps,
@@ -445,6 +451,7 @@ def run_lqg(args, workload):
         "cpu_baseline": cpu,
         "e2e": e2e,
         "sweep": sweep,
+        "moe_grouped": moe,
         "peaks": peaks,
     }
     print(json.dumps(line))
@@ -504,6 +511,69 @@ def run_e2e(args, layers, msweep, xs, world, dev, lqg, ops_step):
             "d2h_bytes_per_step": d2h, "steps": steps,
             "path": "lqg_gemm_w4a8_host (C ABI, pinned host buffers)" if world == 1 else
                     "H2D + lqg_gemm_w4a8 + NCCL all-gather + D2H"}
+
+
+def run_moe(lqg, dev, peaks):
+    """BASELINE config 5: Mixtral-8x7B expert FFN GEMMs (w1/w3 14336x4096, w2
+    4096x14336; 8 experts, top-2 routing of T tokens, seeded skewed router) as
+    ONE grouped launch (lqg_gemm_w4a8_grouped) vs one launch per expert. Device
+    time of CUDA-graph replays (8 x 29 MB of weights per GEMM, > L2 with the
+    rotation below)."""
+    import numpy as np
+    import torch
+    E = 8
+    g = torch.Generator(device=dev)
+    g.manual_seed(42)
+    experts = {nm: [lqg.DeviceWeights.quantize(torch.randn(n, k, generator=g, device=dev) * 0.02, GROUP)
+                    for _ in range(E)] for nm, n, k in (("w1", 14336, 4096), ("w2", 4096, 14336))}
+    ws = lqg.Workspace(dev.index or 0)
+    rng = np.random.default_rng(0)
+
+    def graph_time(fn, reps=8):
+        fn()
+        torch.cuda.synchronize()
+        gr = torch.cuda.CUDAGraph()
+        st = torch.cuda.Stream()
+        st.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(st), torch.cuda.graph(gr, stream=st):
+            for _ in range(reps):
+                fn()
+        torch.cuda.current_stream().wait_stream(st)
+        gr.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        e0.record()
+        gr.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps * 1e-3
+
+    rows_out = []
+    for T in (1, 16, 64, 512, 4096):
+        p = rng.dirichlet(np.full(E, 2.0))
+        ms = np.bincount(rng.choice(E, size=2 * T, p=p), minlength=E).astype(np.uint32).tolist()
+        rows = sum(ms)
+        for nm, dws in experts.items():
+            n, k = dws[0].n, dws[0].k
+            xq, ts = lqg.quantize_activations(torch.randn(rows, k, generator=g, device=dev))
+            y = torch.empty(rows, n, dtype=torch.bfloat16, device=dev)
+            tg = graph_time(lambda: lqg.gemm_grouped(dws, xq, ts, ms, out=y, workspace=ws))
+
+            def per():
+                r0 = 0
+                for dw, m in zip(dws, ms):
+                    if m:
+                        dw.gemm(xq[r0:r0 + m], ts[r0:r0 + m], out=y[r0:r0 + m], workspace=ws)
+                    r0 += m
+            tp_ = graph_time(per)
+            used = [m for m in ms if m]
+            byts = sum(algo_bytes(m, n, k) for m in used)
+            ops = 2 * rows * n * k
+            rows_out.append({"tokens": T, "gemm": nm, "experts_m": ms, "grouped_us": tg * 1e6,
+                             "per_expert_us": tp_ * 1e6, "grouped_tops": ops / tg / 1e12,
+                             "grouped_hbm_frac": byts / tg / 1e9 / peaks["hbm_gbs"],
+                             "grouped_int8_frac": ops / tg / 1e12 / peaks["int8_tops"]})
+    return rows_out
 
 
 def load_profile_summary():
