@@ -434,7 +434,7 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
     p.w_split = std::max(1u, env_u32("LQG_DEBUG_WSPLIT", 1));
     p.pdl_trigger = env_u32("LQG_PDL_TRIGGER", decode ? 2 : 0);
     p.trace_slot = static_cast<uint32_t>(g_launches.load(std::memory_order_relaxed) % 8);
-    const uint32_t budget = decode ? 110 * 1024 - 3072 : 227 * 1024 - 3072;
+    const uint32_t budget = decode ? 110 * 1024 - 5120 : 227 * 1024 - 5120;
     p.stages = std::min<uint32_t>(kMaxStages, budget / p.stage_bytes);
     if (uint32_t st = env_u32("LQG_DEBUG_STAGES", 0)) p.stages = std::min(p.stages, st);
     if (p.stages < 2) return set_err(LQG_EVALIDATION, "tile configuration does not fit shared memory");
@@ -463,7 +463,7 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
         if (uint32_t e = env_u32("LQG_DEBUG_RASTER_GM", 0)) gm = e;
         p.raster_gm = std::max(1u, std::min(gm, MT));
     }
-    const size_t smem = size_t(p.stages) * p.stage_bytes + 1024 + 2048;
+    const size_t smem = size_t(p.stages) * p.stage_bytes + 1024 + 4096;  // ring + align + barriers/misc
 
     DeviceGuard dg(w->device);
     cudaError_t e = cudaSuccess;
