@@ -292,24 +292,19 @@ __device__ __forceinline__ void store_chunk_k(const GemmParams& p, uint32_t m0, 
                                               uint32_t n, const int32_t (&acc)[16], double cs_d,
                                               const double* ts) {
     const uint32_t mend = min(16u, mlim > m0 ? mlim - m0 : 0u);
-    uint64_t idx = uint64_t(m0) * uint64_t(p.ldo) + n;
     // one element to the primary output and every fan-out destination
     auto put = [&](uint64_t i, auto v) {
         using T = decltype(v);
-#ifdef LQG_EXP_NOSTORE
-        if (float(v) != 12345.678f) return;  // timing experiment: compute, do not store
-#endif
         static_cast<T*>(p.out)[i] = v;
         if (kFan)
             for (uint32_t r = 0; r < p.n_fan; ++r) static_cast<T*>(p.fan[r])[i] = v;
     };
-#pragma unroll
-    for (uint32_t j = 0; j < 16; ++j, idx += p.ldo) {
-        if (j >= mend) break;
+    auto one = [&](uint32_t j, uint64_t idx) {
         if (kKind == kOutAcc) {
             put(idx, acc[j]);
         } else {
-            const float y = __double2float_rn(__dmul_rn(__dmul_rn(i32_to_f64_exact(acc[j]), cs_d), ts[j]));
+            const double a = i32_to_f64_exact(acc[j]);
+            const float y = __double2float_rn(__dmul_rn(__dmul_rn(a, cs_d), ts[j]));
             if (kKind == kOutF32)
                 put(idx, y);
             else if (kKind == kOutF16)
@@ -317,6 +312,18 @@ __device__ __forceinline__ void store_chunk_k(const GemmParams& p, uint32_t m0, 
             else
                 put(idx, __float2bfloat16_rn(y));
         }
+    };
+    const uint64_t idx0 = uint64_t(m0) * uint64_t(p.ldo) + n;
+    if (mend == 16) {
+        // full chunk (the common case): branch-free
+#pragma unroll
+        for (uint32_t j = 0; j < 16; ++j) one(j, idx0 + uint64_t(j) * uint64_t(p.ldo));
+    } else {
+        // ragged last chunk: same unrolled body under a predicate (static
+        // register indices, no local-memory copy of acc)
+#pragma unroll
+        for (uint32_t j = 0; j < 16; ++j)
+            if (j < mend) one(j, idx0 + uint64_t(j) * uint64_t(p.ldo));
     }
 }
 
