@@ -371,11 +371,18 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
 
     // Token tile from the largest group; every group gets ceil(m_e / BN) tiles.
     uint32_t MT;
-    const uint32_t BN = choose_bn(max_m, &MT);
+    uint32_t BN = choose_bn(max_m, &MT);
+    // CTA pairs (tcgen05 cta_group::2) for multi-token-tile plain GEMMs: the
+    // two CTAs of a cluster own adjacent weight tiles and each loads half of
+    // the activation tile, halving the per-SM activation SMEM traffic. The
+    // token tile is a multiple of 32 (16 tokens per CTA half).
+    const bool pair = env_u32("LQG_PAIR", 0) && ng == 1 && n_fan == 0 && MT > 1 && G.NT % 2 == 0 &&
+                      w->num_sms >= 2;
+    if (pair) BN = std::min(kMaxTileM, (BN + 31) / 32 * 32);
     CUtensorMap tmap;
     const cuuint64_t dims[2] = {G.k, m};
     const cuuint64_t strides[1] = {cuuint64_t(ldx)};
-    const cuuint32_t box[2] = {kXAtom, BN};
+    const cuuint32_t box[2] = {kXAtom, pair ? BN / 2 : BN};
     const cuuint32_t estr[2] = {1, 1};
     CUresult cr = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(d_x), dims,
                       strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -394,7 +401,7 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
         ge.M = m_list[e];
         ge.MT = (m_list[e] + BN - 1) / BN;
         ge.tile0 = tiles;
-        tiles += ge.MT * G.NT;
+        tiles += ge.MT * (pair ? G.NT / 2 : G.NT);
         row0 += m_list[e];
     }
     gt.n = ng;
@@ -413,14 +420,15 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
     p.flags = reinterpret_cast<uint32_t*>(W->parts + kMaxSlots * kSlotCells);
     p.N = G.n;
     p.KB = G.KB;
-    p.NT = G.NT;
+    p.NT = pair ? G.NT / 2 : G.NT;  // scheduling tiles (pair tiles in pair mode)
+    p.pair = pair ? 1u : 0u;
     p.MT = MT;  // token tiles of the largest group
     p.tiles = tiles;
     p.BN = BN;
     p.P = G.P;
     p.chunk_bytes = G.chunk_bytes;
     p.out_kind = out_kind;
-    p.stage_bytes = (BN * kKBlock + G.chunk_bytes + 1023) / 1024 * 1024;
+    p.stage_bytes = ((pair ? BN / 2 : BN) * kKBlock + G.chunk_bytes + 1023) / 1024 * 1024;
     // Co-resident mode (opt-in, LQG_CORESIDENT=1, single group, small token
     // tiles): <= 110 KB of shared memory, 256 TMEM columns and one dequant
     // warpgroup so that two CTAs fit on an SM and the next GEMM's CTAs are
@@ -448,6 +456,9 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
         std::min<uint64_t>(std::min<uint32_t>(w->num_sms, kMaxSlots), p.total_iters));
     if (uint32_t gd = env_u32("LQG_DEBUG_GRID", 0))
         grid = static_cast<uint32_t>(std::min<uint64_t>({gd, uint64_t(kMaxSlots), p.total_iters}));
+    // pair mode: scheduling units are CTA pairs (grid = 2 x units)
+    const uint32_t units = pair ? std::max(1u, grid / 2) : grid;
+    if (pair) grid = 2 * units;
     // Hybrid schedule: whole-tile rounds first, stream-K over the last G..2G
     // tiles (all tiles when there are fewer than G), tiles rasterized in groups
     // of GM token tiles sized so that the activation and weight slices of one
@@ -455,10 +466,10 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
     {
         const uint64_t T = tiles;
         uint32_t dp = 0;
-        if (!decode && T >= grid && !env_u32("LQG_DEBUG_NO_DP", 0))
-            dp = static_cast<uint32_t>(T % grid == 0 ? T / grid : T / grid - 1);
+        if (!decode && T >= units && !env_u32("LQG_DEBUG_NO_DP", 0))
+            dp = static_cast<uint32_t>(T % units == 0 ? T / units : T / units - 1);
         p.dp_rounds = dp;
-        const double ratio = double(grid) * (kTileN / 2.0) / double(BN);
+        const double ratio = double(units) * ((pair ? 2 : 1) * kTileN / 2.0) / double(BN);
         uint32_t gm = static_cast<uint32_t>(std::lround(std::sqrt(ratio)));
         if (uint32_t e = env_u32("LQG_DEBUG_RASTER_GM", 0)) gm = e;
         p.raster_gm = std::max(1u, std::min(gm, MT));
@@ -479,6 +490,9 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(lqg_w4a8_gemm_kernel<false, kMaxGroups, false>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(lqg_w4a8_gemm_kernel<false, 1, false, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     });
     if (e != cudaSuccess) return set_err(LQG_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
     cudaLaunchConfig_t cfg{};
@@ -486,18 +500,24 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
     cfg.blockDim = dim3(decode ? Roles<true>::kThreadsT : Roles<false>::kThreadsT);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = env_u32("LQG_DEBUG_NO_PDL", 0) ? 0 : 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = pair ? 2 : 1;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pair ? 2 : 1;
     if (ng > 1) {
         LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<false, kMaxGroups, false>, tmap, p, gt));
     } else {
         GroupTable<1> g1{};
         g1.e[0] = gt.e[0];
         g1.n = 1;
-        if (n_fan)
+        if (pair)
+            LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<false, 1, false, true>, tmap, p, g1));
+        else if (n_fan)
             LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<false, 1, true>, tmap, p, g1));
         else if (decode)
             LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<true, 1, false>, tmap, p, g1));

@@ -117,6 +117,9 @@ struct GemmParams {
     uint32_t dp_rounds;        // whole tiles per CTA before the stream-K tail
     uint32_t raster_gm;        // token tiles per raster group
     uint32_t trace_slot;       // LQG_TRACE builds: launch index % 8
+    uint32_t pair;             // 1: CTA pairs (cluster of 2, tcgen05 cta_group::2, M = 256):
+                               //    NT/tiles count pair tiles, each CTA owns weight tile 2*nt+rank
+                               //    and loads half of every activation tile
     uint32_t pdl_trigger;
     uint64_t total_iters;      // tiles*KB
     uint32_t tiles;            // weight-tile x token-tile pairs (summed over groups)
@@ -190,10 +193,14 @@ __device__ __forceinline__ uint32_t range_begin32(uint32_t c, uint32_t G, uint32
 }
 
 // Computed once per CTA (thread 0) and shared through SMEM.
+// Scheduling units: CTAs, or CTA pairs (p.pair).
+__device__ __forceinline__ uint32_t sched_units(const GemmParams& p) {
+    return p.pair ? gridDim.x >> 1 : gridDim.x;
+}
 __device__ __forceinline__ Sched make_sched(const GemmParams& p) {
     Sched s;
-    const uint32_t G = gridDim.x;
-    s.c = blockIdx.x;
+    const uint32_t G = sched_units(p);
+    s.c = p.pair ? blockIdx.x >> 1 : blockIdx.x;
     s.dp_rounds = p.dp_rounds;
     s.sk_tile0 = s.dp_rounds * G;
     s.sk_total = (p.tiles - s.sk_tile0) * p.KB;
@@ -230,7 +237,7 @@ struct Walk {
         kb = 0;
         if (kDP && r < p.dp_rounds) {
             if (++r < p.dp_rounds) {
-                tile += gridDim.x;
+                tile += sched_units(p);
             } else {
                 tile = sk_tile;
                 kb = sk_kb;
@@ -271,7 +278,7 @@ __device__ __forceinline__ TileRef tile_ref(uint32_t t, const GemmParams& p, con
     TileRef r;
     r.wimg = e.wimg;
     r.cs = e.cs;
-    r.nt = nt;
+    r.nt = p.pair ? 2 * nt + ptx::cluster_ctarank() : nt;
     r.row0 = e.row0 + mt * p.BN;
     r.mlim = e.row0 + e.M;
     return r;
@@ -358,7 +365,12 @@ __device__ __forceinline__ void trace(uint32_t slot, uint32_t e) {
 // kFan: the epilogue also stores every tile into p.fan[0..n_fan) (fused
 // all-gather of the N-split driver); a separate instantiation so the plain
 // kernel's epilogue is untouched.
-template <bool kDecode, uint32_t kG, bool kFan>
+// kPair: CTA pairs (cluster of two, tcgen05 cta_group::2, M = 256): each
+// CTA dequantizes its own 128 weight rows into its TMEM and loads half of the
+// activation tile (N/2 tokens); the leader issues one M=256 MMA that reads the
+// B halves from both CTAs' shared memory, which halves the activation
+// shared-memory traffic per SM (the bound at large M).
+template <bool kDecode, uint32_t kG, bool kFan, bool kPair = false>
 __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
     lqg_w4a8_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const GemmParams p,
                          const __grid_constant__ GroupTable<kG> gt) {
@@ -387,11 +399,15 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
     double* ts_s = reinterpret_cast<double*>(misc + 128);  // kMaxBN token scales, as double
 
     const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const uint32_t G = gridDim.x;
+    const uint32_t G = sched_units(p);
     Sched* sched_s = reinterpret_cast<Sched*>(misc + 32);
     const uint32_t KB = p.KB;
     const TmemPlan tp = tmem_plan(p.BN, p.tmem_cols);
-    const uint32_t x_bytes = p.BN * kKBlock;  // activation tile bytes per stage
+    const uint32_t rank = kPair ? ptx::cluster_ctarank() : 0u;  // 0 = pair leader
+    // activation bytes this CTA loads per stage (half of the tile in a pair)
+    const uint32_t x_bytes = (kPair ? p.BN / 2 : p.BN) * kKBlock;
+    // barriers the pair leader waits on, as seen from this CTA
+    auto leader = [&](uint32_t bar) { return kPair ? ptx::mapa(bar, 0) : bar; };
 
     if (threadIdx.x == 0) LQG_T(0);
     if (threadIdx.x == 0) {
@@ -402,20 +418,26 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
             ptx::mbar_init(empty_bar(s), 1);
         }
         for (uint32_t a = 0; a < kMaxASlots; ++a) {
-            ptx::mbar_init(afull_bar(a), Roles<kDecode>::kDQWarps);  // one arrive per dequant warp
+            ptx::mbar_init(afull_bar(a), (kPair ? 2 : 1) * Roles<kDecode>::kDQWarps);  // one arrive per dequant warp
             ptx::mbar_init(aempty_bar(a), 1);
         }
         for (uint32_t a = 0; a < 2; ++a) {
             ptx::mbar_init(accfull_bar(a), 1);
-            ptx::mbar_init(accempty_bar(a), 4);  // one arrive per epilogue warp
+            ptx::mbar_init(accempty_bar(a), kPair ? 8 : 4);  // one arrive per epilogue warp
         }
         ptx::mbar_init(fin_bar, 1);
         ptx::fence_mbar_init();
     }
     if (warp == 0 && lane == 0) ptx::prefetch_tmap(&tmap_x);
-    if (warp == 1) ptx::tmem_alloc(ptx::smem_u32(tmem_holder), p.tmem_cols);
+    if (warp == 1) {
+        if (kPair)
+            ptx::tmem_alloc_pair(ptx::smem_u32(tmem_holder), p.tmem_cols);
+        else
+            ptx::tmem_alloc(ptx::smem_u32(tmem_holder), p.tmem_cols);
+    }
     ptx::tc_fence_before();
     __syncthreads();
+    if (kPair) ptx::cluster_sync();  // the peer's barriers are initialised before any remote arrive
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
     const Sched sch = *sched_s;
@@ -435,7 +457,7 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
         // Activation tiles follow the dependency wait.
         const uint64_t pol_w = p.MT == 1 ? ptx::policy_evict_first() : ptx::policy_evict_last();
         const uint64_t pol_x = ptx::policy_evict_last();
-        const uint32_t atom_bytes = p.BN * kXAtom;
+        const uint32_t atom_bytes = (kPair ? p.BN / 2 : p.BN) * kXAtom;
         // weight walker
         Walk<!kDecode> ww;
         ww.init(sch);
@@ -463,8 +485,22 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
         uint32_t xrow0 = tile_ref(xw.tile, p, gt).row0;
         auto x_issue = [&](uint32_t st) {
             const uint32_t slot = smem_base + st * p.stage_bytes;
+#ifdef LQG_EXP_NOXTMA
+            ptx::mbar_arrive(xfull_bar(st));  // timing experiment: no activation traffic
+            return;
+#endif
+            const int32_t k0 = int32_t(xw.kb * kKBlock);
+            if (kPair) {
+                // both halves count on the leader's barrier; the leader expects the whole tile
+                if (rank == 0) ptx::mbar_arrive_expect_tx(xfull_bar(st), 2 * x_bytes);
+                const int32_t m0 = int32_t(xrow0 + rank * (p.BN / 2));
+                const uint32_t fb = ptx::mapa(xfull_bar(st), 0);
+                ptx::tma_2d_g2s_pair(slot, &tmap_x, k0, m0, fb, pol_x);
+                ptx::tma_2d_g2s_pair(slot + atom_bytes, &tmap_x, k0 + int32_t(kXAtom), m0, fb, pol_x);
+                return;
+            }
             ptx::mbar_arrive_expect_tx(xfull_bar(st), x_bytes);
-            const int32_t k0 = int32_t(xw.kb * kKBlock), m0 = int32_t(xrow0);
+            const int32_t m0 = int32_t(xrow0);
             ptx::tma_2d_g2s(slot, &tmap_x, k0, m0, xfull_bar(st), pol_x);
             ptx::tma_2d_g2s(slot + atom_bytes, &tmap_x, k0 + int32_t(kXAtom), m0, xfull_bar(st),
                             pol_x);
@@ -534,12 +570,12 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
             }
         }
         if (lane == 0 && p.pdl_trigger == 1) ptx::launch_dependents();
-    } else if (warp == 1) {
+    } else if (warp == 1 && (!kPair || rank == 0)) {
         // ------------------------------------------------------------ MMA issuer
-        const uint32_t idesc = ptx::idesc_i8(kTileN, p.BN);
+        const uint32_t idesc = ptx::idesc_i8(kPair ? 2 * kTileN : kTileN, p.BN);
         const uint64_t desc0 = ptx::sw128_kmajor_desc(smem_base);
         const uint32_t stage_desc = p.stage_bytes >> 4;
-        const uint32_t atom_desc = (p.BN * kXAtom) >> 4;
+        const uint32_t atom_desc = ((kPair ? p.BN / 2 : p.BN) * kXAtom) >> 4;
         Walk<!kDecode> mw;
         mw.init(sch);
         bool seg_start = true;
@@ -558,12 +594,23 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
                 const uint64_t bdesc = desc0 + uint64_t(s * stage_desc);
 #pragma unroll
                 for (uint32_t k8 = 0; k8 < kSubBlocks; ++k8)
-                    ptx::mma_i8_ts(d_tmem, a_tmem + k8 * 8,
-                                   bdesc + (k8 / 4) * atom_desc + (k8 % 4) * 2, idesc,
-                                   (seg_start && k8 == 0) ? 0u : 1u);
-                ptx::mma_commit(empty_bar(s));
-                ptx::mma_commit(aempty_bar(a));
-                if (seg_end) ptx::mma_commit(accfull_bar(as));
+                    if (kPair)
+                        ptx::mma_i8_ts_pair(d_tmem, a_tmem + k8 * 8,
+                                            bdesc + (k8 / 4) * atom_desc + (k8 % 4) * 2, idesc,
+                                            (seg_start && k8 == 0) ? 0u : 1u);
+                    else
+                        ptx::mma_i8_ts(d_tmem, a_tmem + k8 * 8,
+                                       bdesc + (k8 / 4) * atom_desc + (k8 % 4) * 2, idesc,
+                                       (seg_start && k8 == 0) ? 0u : 1u);
+                if (kPair) {
+                    ptx::mma_commit_pair(empty_bar(s));
+                    ptx::mma_commit_pair(aempty_bar(a));
+                    if (seg_end) ptx::mma_commit_pair(accfull_bar(as));
+                } else {
+                    ptx::mma_commit(empty_bar(s));
+                    ptx::mma_commit(aempty_bar(a));
+                    if (seg_end) ptx::mma_commit(accfull_bar(as));
+                }
             }
             __syncwarp();
             if (seg_end && ++as == tp.acc_stages) {
@@ -637,7 +684,12 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
             ptx::tmem_st_wait();
             ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(afull_bar(a));
+            if (lane == 0) {
+                if (kPair && rank != 0)
+                    ptx::mbar_arrive_cluster(leader(afull_bar(a)));
+                else
+                    ptx::mbar_arrive(afull_bar(a));
+            }
             if (++s == S) {
                 s = 0;
                 ph ^= 1;
@@ -687,7 +739,8 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
             // [contributor][quad]. Loaded one chunk ahead (software pipeline).
             int4 cb[4][4];
             auto cell_of = [&](uint32_t c, uint32_t ch) {
-                return reinterpret_cast<int4*>(p.parts + uint64_t(c) * kSlotCellsK + (small ? 0u : kSmallCells)) +
+                const uint32_t cs_slot = kPair ? 2 * c + rank : c;  // the matching CTA of a contributor pair
+                return reinterpret_cast<int4*>(p.parts + uint64_t(cs_slot) * kSlotCellsK + (small ? 0u : kSmallCells)) +
                        ch * 4 * kTileN + row;
             };
             auto load_batch = [&](uint32_t c, uint32_t ch) {
@@ -721,7 +774,12 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
                     if (ch + 1 == nchunks) {
                         ptx::tc_fence_before();
                         __syncwarp();
-                        if (lane == 0) ptx::mbar_arrive(accempty_bar(cur_as));
+                        if (lane == 0) {
+                            if (kPair && rank != 0)
+                                ptx::mbar_arrive_cluster(leader(accempty_bar(cur_as)));
+                            else
+                                ptx::mbar_arrive(accempty_bar(cur_as));
+                        }
                     }
                     if (n < p.N) {
                         int32_t a[16];
@@ -744,7 +802,12 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
                     if (ch + 1 == nchunks) {
                         ptx::tc_fence_before();
                         __syncwarp();
-                        if (lane == 0) ptx::mbar_arrive(accempty_bar(cur_as));
+                        if (lane == 0) {
+                            if (kPair && rank != 0)
+                                ptx::mbar_arrive_cluster(leader(accempty_bar(cur_as)));
+                            else
+                                ptx::mbar_arrive(accempty_bar(cur_as));
+                        }
                     }
                     // [chunk][quad q][row] int4 cells: a warp's stores are 512
                     // contiguous bytes, and the finisher's bulk copy is one block
@@ -834,8 +897,9 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
                     const uint32_t nb_max = max(1u, ring_bytes / part_bytes);
                     const int4* sm4 = reinterpret_cast<const int4*>(smem);
                     for (uint32_t c = c_first + et; c < c_end; c += 128) {
-                        while (ptx::ld_acquire_u32(p.flags + c) == 0) __nanosleep(32);
-                        p.flags[c] = 0;
+                        const uint32_t fc = kPair ? 2 * c + rank : c;
+                        while (ptx::ld_acquire_u32(p.flags + fc) == 0) __nanosleep(32);
+                        p.flags[fc] = 0;
                     }
                     asm volatile("bar.sync 1, 128;" ::: "memory");
                     if (et == 0) LQG_T(12);
@@ -847,7 +911,7 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
                             ptx::mbar_arrive_expect_tx(fin_bar, nb * part_bytes);
                             for (uint32_t b = 0; b < nb; ++b)
                                 ptx::bulk_g2s(smem_base + b * part_bytes,
-                                              p.parts + uint64_t(c0 + b) * kSlotCellsK + kSmallCells, part_bytes,
+                                              p.parts + uint64_t(kPair ? 2 * (c0 + b) + rank : c0 + b) * kSlotCellsK + kSmallCells, part_bytes,
                                               fin_bar, ptx::policy_evict_first());
                         }
                         ptx::mbar_wait(fin_bar, fin_ph);
@@ -884,7 +948,12 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
                 }
                 ptx::tc_fence_before();
                 __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(accempty_bar(cur_as));
+                if (lane == 0) {
+                            if (kPair && rank != 0)
+                                ptx::mbar_arrive_cluster(leader(accempty_bar(cur_as)));
+                            else
+                                ptx::mbar_arrive(accempty_bar(cur_as));
+                        }
             }
             asm volatile("bar.sync 1, 128;" ::: "memory");  // ts_s reuse
         }
@@ -895,7 +964,13 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
     __syncthreads();
     ptx::tc_fence_after();
     if (threadIdx.x == 0) LQG_T(8);
-    if (warp == 1) ptx::tmem_dealloc(tmem_base, p.tmem_cols);
+    if (kPair) ptx::cluster_sync();  // the leader's MMAs into this CTA's TMEM are complete
+    if (warp == 1) {
+        if (kPair)
+            ptx::tmem_dealloc_pair(tmem_base, p.tmem_cols);
+        else
+            ptx::tmem_dealloc(tmem_base, p.tmem_cols);
+    }
 }
 
 }  // namespace lqg

@@ -401,3 +401,22 @@ def test_column_parallel_p2p_single_rank(torch_cuda, lqg):
     except Exception as exc:  # symmetric memory needs a distributed backend on some builds
         pytest.skip(f"symmetric memory unavailable: {exc}")
     assert torch.equal(y, layer.dw.gemm(q, ts))
+
+
+@pytest.mark.parametrize("m,n,k", [(400, 256, 1024), (1000, 2048, 4096), (4096, 1024, 8192), (300, 384, 640)])
+def test_cta_pair_mode_matches(torch_cuda, lqg, m, n, k):
+    """Opt-in CTA-pair kernel (LQG_PAIR=1: cluster of two, tcgen05 cta_group::2,
+    M = 256, each CTA loading half of every activation tile) is bit-identical
+    to the one-CTA kernel (accumulators and BF16)."""
+    torch = torch_cuda
+    g = torch.Generator(device="cuda").manual_seed(m + n)
+    dw = lqg.DeviceWeights.quantize(torch.randn(n, k, generator=g, device="cuda") * 0.02, 128)
+    q, ts = lqg.quantize_activations(torch.randn(m, k, generator=g, device="cuda"))
+    acc0, y0 = dw.gemm_accum(q), dw.gemm(q, ts)
+    os.environ["LQG_PAIR"] = "1"
+    try:
+        acc1, y1 = dw.gemm_accum(q), dw.gemm(q, ts)
+        torch.cuda.synchronize()
+    finally:
+        del os.environ["LQG_PAIR"]
+    assert torch.equal(acc0, acc1) and torch.equal(y0, y1)
