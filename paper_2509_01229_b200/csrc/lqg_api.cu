@@ -509,6 +509,29 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
     attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pair ? 2 : 1;
+    if (pair) {
+        // Not every SM can host half of a 2-CTA cluster (GPC / TPC boundaries):
+        // size the persistent grid to the clusters that are co-resident, so no
+        // pair runs in a second wave.
+        static thread_local size_t cached_smem = 0;
+        static thread_local int cached_clusters = 0;
+        if (cached_smem != smem) {
+            int nc = 0;
+            if (cudaOccupancyMaxActiveClusters(&nc, lqg_w4a8_gemm_kernel<false, 1, false, true>, &cfg) != cudaSuccess)
+                nc = 0;
+            cudaGetLastError();
+            cached_smem = smem;
+            cached_clusters = nc;
+        }
+        if (cached_clusters > 0 && uint32_t(cached_clusters) < grid / 2) {
+            // re-derive the schedule for fewer pairs
+            const uint32_t u = uint32_t(cached_clusters);
+            cfg.gridDim = dim3(2 * u);
+            const uint64_t T = tiles;
+            p.dp_rounds = (T >= u && !env_u32("LQG_DEBUG_NO_DP", 0))
+                              ? static_cast<uint32_t>(T % u == 0 ? T / u : T / u - 1) : 0;
+        }
+    }
     if (ng > 1) {
         LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<false, kMaxGroups, false>, tmap, p, gt));
     } else {
