@@ -440,6 +440,7 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
     // ~24 MB of weights across the grid (enough to cover a kernel tail at HBM rate).
     p.l2_prefetch = env_u32("LQG_L2_PREFETCH_CHUNKS", decode ? 4 : 0);
     p.w_split = std::max(1u, env_u32("LQG_DEBUG_WSPLIT", 1));
+    p.l2_last = env_u32("LQG_L2_EVICT_LAST", 1);
     p.pdl_trigger = env_u32("LQG_PDL_TRIGGER", decode ? 2 : 0);
     p.trace_slot = static_cast<uint32_t>(g_launches.load(std::memory_order_relaxed) % 8);
     const uint32_t budget = decode ? 110 * 1024 - 5120 : 227 * 1024 - 5120;

@@ -117,6 +117,7 @@ struct GemmParams {
     uint32_t dp_rounds;        // whole tiles per CTA before the stream-K tail
     uint32_t raster_gm;        // token tiles per raster group
     uint32_t trace_slot;       // LQG_TRACE builds: launch index % 8
+    uint32_t l2_last;          // 1: EVICT_LAST cache hints for reused tiles (default)
     uint32_t pair;             // 1: CTA pairs (cluster of 2, tcgen05 cta_group::2, M = 256):
                                //    NT/tiles count pair tiles, each CTA owns weight tile 2*nt+rank
                                //    and loads half of every activation tile
@@ -455,8 +456,12 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
         // chunks are in flight before griddepcontrol.wait, so the weight
         // stream of this GEMM overlaps the tail of the previous kernel.
         // Activation tiles follow the dependency wait.
-        const uint64_t pol_w = p.MT == 1 ? ptx::policy_evict_first() : ptx::policy_evict_last();
-        const uint64_t pol_x = ptx::policy_evict_last();
+        // Reused tiles (activations; weights re-read by several token tiles)
+        // EVICT_LAST, a single-pass weight stream EVICT_FIRST. (Normal
+        // priority via LQG_L2_EVICT_LAST=0 measured ~2 % slower at M = 4096.)
+        const uint64_t pol_w = p.MT == 1 ? ptx::policy_evict_first()
+                                         : (p.l2_last ? ptx::policy_evict_last() : ptx::policy_evict_normal());
+        const uint64_t pol_x = p.l2_last ? ptx::policy_evict_last() : ptx::policy_evict_normal();
         const uint32_t atom_bytes = (kPair ? p.BN / 2 : p.BN) * kXAtom;
         // weight walker
         Walk<!kDecode> ww;
