@@ -315,6 +315,8 @@ constexpr uint32_t kMaxTileM = 192;
 // Token tiles up to this size run in decode mode (see launch_gemm).
 constexpr uint32_t kDecodeMaxBN = 32;
 
+constexpr uint32_t kPairMinM = 320;  // auto CTA-pair threshold (tokens)
+
 uint32_t env_u32(const char* name, uint32_t dflt) {
     const char* v = std::getenv(name);
     return v && *v ? static_cast<uint32_t>(std::strtoul(v, nullptr, 10)) : dflt;
@@ -375,9 +377,13 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
     // CTA pairs (tcgen05 cta_group::2) for multi-token-tile plain GEMMs: the
     // two CTAs of a cluster own adjacent weight tiles and each loads half of
     // the activation tile, halving the per-SM activation SMEM traffic. The
-    // token tile is a multiple of 32 (16 tokens per CTA half).
-    const bool pair = env_u32("LQG_PAIR", 0) && ng == 1 && n_fan == 0 && MT > 1 && G.NT % 2 == 0 &&
-                      w->num_sms >= 2;
+    // token tile is a multiple of 32 (16 tokens per CTA half). Default: on from
+    // kPairMinM tokens (LLaMA-2-70B 4-GEMM step on B200: -6 % at M = 320,
+    // -5 % at 1024, -12 % at 8192, but +6 % at 256); LQG_PAIR=0 / 1 forces it
+    // off / on.
+    const uint32_t pair_mode = env_u32("LQG_PAIR", 2);
+    const bool pair = (pair_mode == 1 || (pair_mode == 2 && m >= env_u32("LQG_PAIR_MIN_M", kPairMinM))) &&
+                      ng == 1 && n_fan == 0 && MT > 1 && G.NT % 2 == 0 && w->num_sms >= 2;
     if (pair) BN = std::min(kMaxTileM, (BN + 31) / 32 * 32);
     CUtensorMap tmap;
     const cuuint64_t dims[2] = {G.k, m};

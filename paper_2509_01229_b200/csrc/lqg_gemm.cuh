@@ -585,13 +585,32 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
         mw.init(sch);
         bool seg_start = true;
         uint32_t s = 0, ph = 0, a = 0, aph = 0, as = 0, acc_ph = 0;
+#ifdef LQG_TRACE
+        long long w_acc = 0, w_a = 0, w_x = 0;
+        const long long t_mma0 = clock64();
+#endif
         for (uint32_t i = 0; i < n_local; ++i) {
             const bool seg_end = (mw.kb == KB - 1) || (i + 1 == n_local);
+#ifdef LQG_TRACE
+            const long long tw0 = clock64();
+            if (seg_start) ptx::mbar_wait(accempty_bar(as), acc_ph ^ 1);
+            const long long tw1 = clock64();
+            ptx::mbar_wait(afull_bar(a), aph);
+            const long long tw2 = clock64();
+            ptx::mbar_wait(xfull_bar(s), ph);
+            const long long tw3 = clock64();
+            w_acc += tw1 - tw0;
+            w_a += tw2 - tw1;
+            w_x += tw3 - tw2;
+#else
             if (seg_start) ptx::mbar_wait(accempty_bar(as), acc_ph ^ 1);
             ptx::mbar_wait(afull_bar(a), aph);
             ptx::mbar_wait(xfull_bar(s), ph);
+#endif
+#ifndef LQG_TRACE_DQ
             if (i == 0 && lane == 0) LQG_T(4);
             if (i + 1 == n_local && lane == 0) LQG_T(5);
+#endif
             ptx::tc_fence_after();
             if (ptx::elect_one()) {
                 const uint32_t d_tmem = tmem_base + as * tp.acc_stride;
@@ -633,6 +652,14 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
             }
         }
         if (lane == 0 && p.pdl_trigger == 2) ptx::launch_dependents();
+#ifdef LQG_TRACE
+        if (lane == 0) {  // MMA-warp wait cycles: accumulator, A operand, activation tile, total
+            LQG_TV(12, (unsigned long long)w_acc);
+            LQG_TV(13, (unsigned long long)w_a);
+            LQG_TV(14, (unsigned long long)w_x);
+            LQG_TV(15, (unsigned long long)(clock64() - t_mma0));
+        }
+#endif
     } else if (warp >= kDequantWarp0 && warp < Roles<kDecode>::kEpi0) {
         // ------------------------------------------------------------ dequant WGs
         // Both warpgroups work on every k-block: WG w dequantizes sub-blocks
@@ -645,12 +672,25 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
         const uint32_t p_shift = param_shift(p.P);
         constexpr uint32_t kHalf = kSubBlocks / (Roles<kDecode>::kDQWarps / 4);  // sub-blocks per WG
         uint32_t s = 0, ph = 0, a = 0, aph = 0;
+#ifdef LQG_TRACE
+        long long dq_w = 0, dq_a = 0, dq_st = 0, dq_ar = 0;
+        const long long t_dq0 = clock64();
+#endif
         const uint8_t* ring_w = smem + x_bytes;
         const uint32_t a_base = tmem_base + lane_addr + tp.a_base + wg * kHalf * 8;
         for (uint32_t i = 0; i < n_local; ++i) {
+#ifdef LQG_TRACE
+            const long long td0 = clock64();
             ptx::mbar_wait(wfull_bar(s), ph);
-            if (i == 0 && warp == kDequantWarp0 && lane == 0) LQG_T(3);
+            const long long td1 = clock64();
             ptx::mbar_wait(aempty_bar(a), aph ^ 1);
+            const long long td2 = clock64();
+            dq_w += td1 - td0;
+            dq_a += td2 - td1;
+#else
+            ptx::mbar_wait(wfull_bar(s), ph);
+            ptx::mbar_wait(aempty_bar(a), aph ^ 1);
+#endif
             ptx::tc_fence_after();
             const uint8_t* wchunk = ring_w + s * p.stage_bytes;
             const uint16_t* prm = reinterpret_cast<const uint16_t*>(wchunk + kCodeBytes);
@@ -686,15 +726,26 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
 #endif
                 ptx::tmem_st_x8(a_taddr + cc * 8, o);
             }
+#ifdef LQG_TRACE
+            const long long td3 = clock64();
+#endif
             ptx::tmem_st_wait();
+#ifdef LQG_TRACE
+            const long long td4 = clock64();
+#endif
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) {
                 if (kPair && rank != 0)
-                    ptx::mbar_arrive_cluster(leader(afull_bar(a)));
+                    ptx::mbar_arrive_cluster_relaxed(leader(afull_bar(a)));
                 else
                     ptx::mbar_arrive(afull_bar(a));
             }
+#ifdef LQG_TRACE
+            __syncwarp();
+            dq_st += td4 - td3;
+            dq_ar += clock64() - td4;
+#endif
             if (++s == S) {
                 s = 0;
                 ph ^= 1;
@@ -704,6 +755,17 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
                 aph ^= 1;
             }
         }
+#ifdef LQG_TRACE
+        if (warp == kDequantWarp0 && lane == 0) {  // dequant waits: weights, A slot, total
+            LQG_TV(2, (unsigned long long)dq_w);
+            LQG_TV(3, (unsigned long long)dq_a);
+#ifdef LQG_TRACE_DQ
+            LQG_TV(4, (unsigned long long)dq_st);
+            LQG_TV(5, (unsigned long long)dq_ar);
+#endif
+            LQG_TV(11, (unsigned long long)(clock64() - t_dq0));
+        }
+#endif
     } else if (warp >= Roles<kDecode>::kEpi0) {
         // ------------------------------------------------------------ epilogue
         const uint32_t sp = warp % 4;
@@ -781,7 +843,7 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
                         __syncwarp();
                         if (lane == 0) {
                             if (kPair && rank != 0)
-                                ptx::mbar_arrive_cluster(leader(accempty_bar(cur_as)));
+                                ptx::mbar_arrive_cluster_relaxed(leader(accempty_bar(cur_as)));
                             else
                                 ptx::mbar_arrive(accempty_bar(cur_as));
                         }
@@ -809,7 +871,7 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
                         __syncwarp();
                         if (lane == 0) {
                             if (kPair && rank != 0)
-                                ptx::mbar_arrive_cluster(leader(accempty_bar(cur_as)));
+                                ptx::mbar_arrive_cluster_relaxed(leader(accempty_bar(cur_as)));
                             else
                                 ptx::mbar_arrive(accempty_bar(cur_as));
                         }
@@ -907,7 +969,7 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
                         p.flags[fc] = 0;
                     }
                     asm volatile("bar.sync 1, 128;" ::: "memory");
-                    if (et == 0) LQG_T(12);
+                    (void)0;
                     for (uint32_t c0 = c_first; c0 < c_end; c0 += nb_max) {
                         const uint32_t nb = min(nb_max, c_end - c0);
                         const bool last_batch = c0 + nb >= c_end;
@@ -955,7 +1017,7 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
                 __syncwarp();
                 if (lane == 0) {
                             if (kPair && rank != 0)
-                                ptx::mbar_arrive_cluster(leader(accempty_bar(cur_as)));
+                                ptx::mbar_arrive_cluster_relaxed(leader(accempty_bar(cur_as)));
                             else
                                 ptx::mbar_arrive(accempty_bar(cur_as));
                         }

@@ -403,20 +403,50 @@ def test_column_parallel_p2p_single_rank(torch_cuda, lqg):
     assert torch.equal(y, layer.dw.gemm(q, ts))
 
 
-@pytest.mark.parametrize("m,n,k", [(400, 256, 1024), (1000, 2048, 4096), (4096, 1024, 8192), (300, 384, 640)])
+def _with_env(name, value, fn):
+    old = os.environ.get(name)
+    os.environ[name] = value
+    try:
+        return fn()
+    finally:
+        if old is None:
+            del os.environ[name]
+        else:
+            os.environ[name] = old
+
+
+@pytest.mark.parametrize("m,n,k", [(400, 256, 1024), (1000, 2048, 4096), (4096, 1024, 8192), (300, 384, 640),
+                                   (8192, 512, 1024), (333, 8192, 1024)])
 def test_cta_pair_mode_matches(torch_cuda, lqg, m, n, k):
-    """Opt-in CTA-pair kernel (LQG_PAIR=1: cluster of two, tcgen05 cta_group::2,
-    M = 256, each CTA loading half of every activation tile) is bit-identical
-    to the one-CTA kernel (accumulators and BF16)."""
+    """CTA-pair kernel (cluster of two, tcgen05 cta_group::2, M = 256, each
+    CTA loading half of every activation tile; the default from 320 tokens)
+    is bit-identical to the one-CTA kernel (LQG_PAIR=0), accumulators and BF16."""
     torch = torch_cuda
     g = torch.Generator(device="cuda").manual_seed(m + n)
     dw = lqg.DeviceWeights.quantize(torch.randn(n, k, generator=g, device="cuda") * 0.02, 128)
     q, ts = lqg.quantize_activations(torch.randn(m, k, generator=g, device="cuda"))
-    acc0, y0 = dw.gemm_accum(q), dw.gemm(q, ts)
-    os.environ["LQG_PAIR"] = "1"
-    try:
-        acc1, y1 = dw.gemm_accum(q), dw.gemm(q, ts)
+
+    def run():
+        r = dw.gemm_accum(q), dw.gemm(q, ts)
         torch.cuda.synchronize()
-    finally:
-        del os.environ["LQG_PAIR"]
+        return r
+    acc0, y0 = _with_env("LQG_PAIR", "0", run)
+    acc1, y1 = _with_env("LQG_PAIR", "1", run)
     assert torch.equal(acc0, acc1) and torch.equal(y0, y1)
+
+
+@pytest.mark.parametrize("m,n,k,g", [(320, 256, 512, 128), (517, 512, 768, 64), (1100, 256, 1024, 256)])
+def test_cta_pair_mode_matches_oracle(torch_cuda, lqg, port, m, n, k, g):
+    """Default-path pair kernel against the CPU oracle (gemm.cpp:225-243,
+    quant.cpp:125-127): INT32 bit-exact, F32 bit-identical, ragged token tail."""
+    torch = torch_cuda
+    rng = np.random.default_rng(m + n + k)
+    b = port.build_bundle_plain(make_weights(rng, n, k), g)
+    dw = lqg.DeviceWeights.from_bundle(to_bundle(lqg, b), 0)
+    q, ts = port.quantize_activations(make_acts(rng, m, k))
+    acc_ref, y_ref = port.gemm_oracle(q, ts, port.bundle_int8(b), b["channel_scales"])
+    xq, tsd = torch.from_numpy(q).cuda(), torch.from_numpy(ts).cuda()
+    acc = _with_env("LQG_PAIR", "1", lambda: dw.gemm_accum(xq).cpu().numpy())
+    y = _with_env("LQG_PAIR", "1", lambda: dw.gemm(xq, tsd, out_dtype=torch.float32).cpu().numpy())
+    np.testing.assert_array_equal(acc.astype(np.int64), acc_ref)
+    np.testing.assert_array_equal(y.view(np.uint32), y_ref.view(np.uint32))

@@ -1,1 +1,2 @@
-timeout 900 python bench.py --no-cpu-baseline --no-e2e 2>/dev/null | python -c "import json,sys; d=json.loads([l for l in sys.stdin if l.startswith('{')][-1]); print(round(d['value']), round(d['roofline_decode']['frac'],3), round(d['roofline']['frac'],3), [(r['m'], round(r['us'],1)) for r in d['sweep']])"
+python -m pytest tests -m gpu -q -x 2>&1 | tail -3
+python bench.py > gpurun_out/bench_pair.log 2> gpurun_out/bench_pair.err; tail -c 3000 gpurun_out/bench_pair.log
