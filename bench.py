@@ -68,6 +68,8 @@ def load_peaks():
         ip = json.load(open(p))
         peaks["int8_tops"] = float(ip["int8_tops"])
         peaks["int8_src"] = "measured cuBLASLt IMMA burst (profiles/int8_peak.json)"
+        if "int8_tops_sustained" in ip:
+            peaks["int8_tops_sustained"] = float(ip["int8_tops_sustained"])
     return peaks
 
 
@@ -373,12 +375,36 @@ def run_lqg(args, workload):
                 torch.cuda.synchronize()
                 samples.append(e0.elapsed_time(e1) * 1e-3 / (reps * R))
             t_s = statistics.median(samples)
+            if m == mmax:
+                # The tensor-bound entry in both power states (B200 board limit
+                # 1000 W: after seconds of back-to-back INT8 MMA the SM clock
+                # settles near 1450 MHz, sw_power_cap). Burst: after 2 s idle,
+                # 5 replays (~30 ms). Sustained: after 6 s of continuous replays.
+                # Each is compared with the matching cuBLASLt IMMA peak.
+                states = {}
+                for state, pre in (("burst", 0.0), ("sustained", 6.0)):
+                    time.sleep(2.0)
+                    t0 = time.time()
+                    while time.time() - t0 < pre:
+                        for _ in range(10):
+                            g.replay()
+                        torch.cuda.synchronize()
+                    with ClockSampler(local, 0.002) as ck:
+                        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                        e0.record()
+                        for _ in range(5):
+                            g.replay()
+                        e1.record()
+                        torch.cuda.synchronize()
+                    states[state] = {"us": e0.elapsed_time(e1) * 1e-3 / (5 * R) * 1e6, "clocks": ck.result()}
             ops = sum(algo_ops(m, L["n"], L["k"]) for L in layers)
             byts = sum(algo_bytes(m, L["n"], L["k"]) for L in layers)
             sweep.append({"m": m, "us": t_s * 1e6, "tops": ops / t_s / 1e12,
                           "hbm_gbs": byts / t_s / 1e9,
                           "hbm_frac": byts / t_s / 1e9 / peaks["hbm_gbs"],
                           "int8_frac": ops / t_s / 1e12 / peaks["int8_tops"]})
+            if m == mmax:
+                sweep[-1]["power_states"] = states
             del g
 
     # ---- e2e through the reference-facing host-buffer C-ABI call
@@ -421,11 +447,21 @@ def run_lqg(args, workload):
     roofline = roofline_decode = None
     prof = load_profile_summary()
     big = pick(mmax)
-    if big:
-        roofline = {"bound": "tensor", "achieved": big["tops"], "peak": peaks["int8_tops"],
-                    "unit": "TFLOP/s", "frac": big["tops"] / peaks["int8_tops"],
+    if big and "power_states" in big:
+        ops = sum(algo_ops(mmax, L["n"], L["k"]) for L in layers)
+        st = big["power_states"]
+        burst = ops / (st["burst"]["us"] * 1e-6) / 1e12
+        sust = ops / (st["sustained"]["us"] * 1e-6) / 1e12
+        roofline = {"bound": "tensor", "achieved": burst, "peak": peaks["int8_tops"],
+                    "unit": "TFLOP/s", "frac": burst / peaks["int8_tops"],
                     "traffic": prof.get("traffic_bytes_M4096"),
-                    "at": f"M={mmax}, 4 layer GEMMs, INT8 ops (TOPS)", "peak_src": peaks["int8_src"]}
+                    "at": f"M={mmax}, 4 layer GEMMs, INT8 ops (TOPS), burst: timed 2 s after idle",
+                    "peak_src": peaks["int8_src"], "clocks": st["burst"]["clocks"],
+                    "sustained": {"achieved": sust, "peak": peaks.get("int8_tops_sustained"),
+                                  "frac": sust / peaks["int8_tops_sustained"] if peaks.get("int8_tops_sustained") else None,
+                                  "at": "after 6 s of back-to-back replays (power-capped)",
+                                  "clocks": st["sustained"]["clocks"]},
+                    "sweep_entry": {"achieved": big["tops"], "note": "median of 7 inside the sweep (partly power-capped)"}}
     small = pick(16)
     if small:
         roofline_decode = {"bound": "hbm", "achieved": small["hbm_gbs"], "peak": peaks["hbm_gbs"],
