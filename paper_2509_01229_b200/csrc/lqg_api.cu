@@ -382,8 +382,9 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
     // -5 % at 1024, -12 % at 8192, but +6 % at 256); LQG_PAIR=0 / 1 forces it
     // off / on.
     const uint32_t pair_mode = env_u32("LQG_PAIR", 2);
-    const bool pair = (pair_mode == 1 || (pair_mode == 2 && m >= env_u32("LQG_PAIR_MIN_M", kPairMinM))) &&
-                      ng == 1 && n_fan == 0 && MT > 1 && G.NT % 2 == 0 && w->num_sms >= 2;
+    // Grouped launches decide on the largest group (its token tiles dominate).
+    const bool pair = (pair_mode == 1 || (pair_mode == 2 && max_m >= env_u32("LQG_PAIR_MIN_M", kPairMinM))) &&
+                      n_fan == 0 && MT > 1 && G.NT % 2 == 0 && w->num_sms >= 2;
     if (pair) BN = std::min(kMaxTileM, (BN + 31) / 32 * 32);
     CUtensorMap tmap;
     const cuuint64_t dims[2] = {G.k, m};
@@ -500,6 +501,9 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(lqg_w4a8_gemm_kernel<false, 1, false, true>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(lqg_w4a8_gemm_kernel<false, kMaxGroups, false, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     });
     if (e != cudaSuccess) return set_err(LQG_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
     cudaLaunchConfig_t cfg{};
@@ -540,7 +544,10 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
         }
     }
     if (ng > 1) {
-        LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<false, kMaxGroups, false>, tmap, p, gt));
+        if (pair)
+            LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<false, kMaxGroups, false, true>, tmap, p, gt));
+        else
+            LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<false, kMaxGroups, false>, tmap, p, gt));
     } else {
         GroupTable<1> g1{};
         g1.e[0] = gt.e[0];
