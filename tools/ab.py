@@ -5,7 +5,7 @@ import argparse, json, os, subprocess, sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CHILD = r'''
-import os, sys, json
+import os, sys, json, time
 sys.path.insert(0, ROOT)
 import torch
 import paper_2509_01229_b200 as lqg
@@ -28,6 +28,7 @@ for m in ms:
         for _ in range(3): step()
     torch.cuda.current_stream().wait_stream(s)
     gr.replay(); torch.cuda.synchronize()
+    time.sleep(IDLE)  # burst state: after idle (B200 power-caps within ~1 s of heavy MMA)
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
     e0.record()
     for _ in range(5): gr.replay()
@@ -41,6 +42,7 @@ def main():
     ap.add_argument("--libs", required=True)
     ap.add_argument("--ms", default="16")
     ap.add_argument("--rounds", type=int, default=3)
+    ap.add_argument("--idle", type=float, default=1.5, help="seconds idle before each timing")
     ap.add_argument("--env", default="", help="extra env per lib, ';'-separated list of k=v,k=v")
     a = ap.parse_args()
     libs = a.libs.split(",")
@@ -53,7 +55,7 @@ def main():
             for kv in filter(None, envs[i].split(",")):
                 k, v = kv.split("=")
                 env[k] = v
-            code = CHILD.replace("ROOT", repr(ROOT)).replace("MS", repr(ms))
+            code = CHILD.replace("ROOT", repr(ROOT)).replace("MS", repr(ms)).replace("IDLE", repr(a.idle))
             o = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
             if o.returncode:
                 print(lib, "FAILED", o.stderr[-500:]); continue

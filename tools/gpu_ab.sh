@@ -1,4 +1,2 @@
-python -m pytest tests -m gpu -q -x 2>&1 | tail -3
 P=paper_2509_01229_b200/liblqg.so
-LQG_PAIR=0 python tools/moe_time.py 2>&1 | tail -12
-python tools/moe_time.py 2>&1 | tail -12
+python tools/ab.py --libs $P,$P,$P --env "LQG_DEBUG_MAX_BN=192;LQG_DEBUG_MAX_BN=224;LQG_DEBUG_MAX_BN=208" --ms 1024,2048,4096,8192 --rounds 2

@@ -3,7 +3,7 @@
 mkdir -p gpurun_out/ncu
 for s in "10240 8192" "8192 8192" "28672 8192" "8192 28672"; do
   set -- $s
-  for m in 16 4096; do
+  for m in ${MS:-16 4096}; do
     timeout 600 ncu --set full --clock-control none -k regex:lqg_w4a8 -s 2 -c 1 -o gpurun_out/ncu/prof_${1}x${2}_m$m python tools/profile_one.py --n $1 --k $2 --m $m > /dev/null 2>&1; echo "ncu $1x$2 m=$m rc=$?"
     B=$(python -c "n,k,m=$1,$2,$m; print(n*k//2+2*n*k//128+4*n+m*k+4*m+2*m*n)"); O=$(python -c "print(2*$m*$1*$2)")
     python tools/ncu_summary.py rep gpurun_out/ncu/prof_${1}x${2}_m$m.ncu-rep --bytes $B --ops $O > gpurun_out/r_ncu_${1}x${2}_m$m.json
