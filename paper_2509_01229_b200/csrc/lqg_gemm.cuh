@@ -755,14 +755,12 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
                 aph ^= 1;
             }
         }
-#ifdef LQG_TRACE
+#ifdef LQG_TRACE_DQ  // (with LQG_TRACE) replaces the timeline slots 2-5 and 11
         if (warp == kDequantWarp0 && lane == 0) {  // dequant waits: weights, A slot, total
             LQG_TV(2, (unsigned long long)dq_w);
             LQG_TV(3, (unsigned long long)dq_a);
-#ifdef LQG_TRACE_DQ
             LQG_TV(4, (unsigned long long)dq_st);
             LQG_TV(5, (unsigned long long)dq_ar);
-#endif
             LQG_TV(11, (unsigned long long)(clock64() - t_dq0));
         }
 #endif

@@ -70,3 +70,14 @@ for li, sl in enumerate(slots):
               f"acc {rel[i,6]:6.2f} end {rel[i,7]:6.2f} pub {rel[i,9] if t[i,9] else -1:6.2f} fin_first {fl:6.2f} "
               f"spins {int(t[i,13])} contrib [{cf},{ce})"
               + "".join(f" | c{c}: entry {rel[c,0]:.2f} pub {rel[c,9]:.2f}" for c in range(cf, ce) if c < len(rel)))
+
+# lateness vs blockIdx: median (over buckets of 16 CTAs) of entry and mma_last
+print(" entry / mma_last / exit by blockIdx bucket of 16 (us):")
+for li, sl in enumerate(slots):
+    t = raw[sl]
+    rel = (t[:, :11] - t0) / 1000.0
+    row = []
+    for b in range(0, 148, 16):
+        r = rel[b:min(b + 16, 148)]
+        row.append(f"{np.median(r[:,0]):5.1f}/{np.median(r[:,5]):5.1f}/{np.median(r[:,8]):5.1f}")
+    print(f"  layer {li}: " + " ".join(row))
