@@ -821,7 +821,7 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
                 if (small) load_batch(c_first, 0);
             }
             asm volatile("bar.sync 1, 128;" ::: "memory");
-            ptx::mbar_wait(accfull_bar(as), acc_ph);
+            ptx::mbar_wait_parked(accfull_bar(as), acc_ph);  // idle for a tile mainloop
             if (i >= n_local && et == 0) LQG_T(6);
             ptx::tc_fence_after();
             const uint32_t acc_taddr = tmem_base + lane_addr + as * tp.acc_stride;

@@ -63,6 +63,23 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         : "memory");
 }
 
+// Long waits (epilogue warps idle for a whole tile mainloop): try_wait with a
+// suspend-time hint parks the warp until the phase completes (or the hint
+// elapses) instead of re-issuing try_wait/branch, which would take issue slots
+// from the dequant warps sharing its SM sub-partition.
+__device__ __forceinline__ void mbar_wait_parked(uint32_t bar, uint32_t parity) {
+#ifndef LQG_PARK_NS
+#define LQG_PARK_NS 1000000
+#endif
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "LQG_PWAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra LQG_PWAIT_%=;\n\t}" ::"r"(bar),
+        "r"(parity), "n"(LQG_PARK_NS)
+        : "memory");
+}
+
 // ---------------------------------------------------------------- global memory
 // Re-read of four 32-bit words at GPU scope (each element single-copy atomic,
 // not served from L1): used to spin on split-K cells.
