@@ -450,3 +450,15 @@ def test_cta_pair_mode_matches_oracle(torch_cuda, lqg, port, m, n, k, g):
     y = _with_env("LQG_PAIR", "1", lambda: dw.gemm(xq, tsd, out_dtype=torch.float32).cpu().numpy())
     np.testing.assert_array_equal(acc.astype(np.int64), acc_ref)
     np.testing.assert_array_equal(y.view(np.uint32), y_ref.view(np.uint32))
+
+
+def test_pair_threshold_boundary_is_seamless(torch_cuda, lqg):
+    """m = 319 (one-CTA kernel) and m = 320 (pair kernel by default) agree on
+    their common rows: the automatic switch never changes results."""
+    torch = torch_cuda
+    g = torch.Generator(device="cuda").manual_seed(319)
+    dw = lqg.DeviceWeights.quantize(torch.randn(1024, 2048, generator=g, device="cuda") * 0.02, 128)
+    q, ts = lqg.quantize_activations(torch.randn(320, 2048, generator=g, device="cuda"))
+    a319, y319 = dw.gemm_accum(q[:319]), dw.gemm(q[:319], ts[:319])
+    a320, y320 = dw.gemm_accum(q), dw.gemm(q, ts)
+    assert torch.equal(a319, a320[:319]) and torch.equal(y319, y320[:319])
