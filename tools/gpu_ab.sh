@@ -1,2 +1,3 @@
+LQG_UA=1 timeout 600 python -m pytest tests -m gpu -q -x 2>&1 | tail -3
 P=paper_2509_01229_b200/liblqg.so
-python tools/ab.py --libs $P,$P,$P,$P,$P --env "LQG_DEBUG_STAGES=16;LQG_DEBUG_STAGES=8;LQG_DEBUG_STAGES=6;LQG_DEBUG_STAGES=4;LQG_DEBUG_STAGES=3" --ms 16,64,128 --rounds 2
+python tools/ab.py --libs $P,$P --env "LQG_UA=0;LQG_UA=1" --ms 1,16,32,64 --rounds 3
