@@ -147,9 +147,16 @@ int lqg_weights_export(const lqg_weights* w, uint8_t* packed, uint8_t* group_sca
  * channel scales): the weight term of the roofline. */
 uint64_t lqg_weights_device_bytes(const lqg_weights* w);
 
-/* Split-K workspace. A handle owns a default one, which makes concurrent
- * launches that share a handle unsafe; pass your own per stream instead.
- * Workspaces are zero on creation and left zero by every launch. */
+/* Split-K workspace (~23.6 MB of device memory). Passing ws = NULL uses the
+ * default workspace of the (device, stream) pair: shared by every handle,
+ * created on the first launch on that stream (one synchronous
+ * initialisation, legal during CUDA-graph capture) and kept for the life of
+ * the process. Launches on one stream are ordered, so they may share it;
+ * launches on different streams get different ones. A graph captured on a
+ * stream uses that stream's workspace: do not replay it concurrently with
+ * other launches captured on or issued to the same stream without passing an
+ * explicit workspace. Workspaces are initialised on creation and left in
+ * that state by every launch. */
 typedef struct lqg_workspace lqg_workspace;
 int lqg_workspace_create(int device, lqg_workspace** out);
 int lqg_workspace_destroy(lqg_workspace* ws);
@@ -159,7 +166,7 @@ int lqg_workspace_destroy(lqg_workspace* ws);
  *   d_x: m rows of int8 codes, row pitch ldx bytes (ldx % 16 == 0, ldx >= k).
  *   d_token_scales: m floats.
  *   d_y: m rows, row pitch ldy elements of y_dtype.
- *   ws: NULL = the handle's workspace.
+ *   ws: NULL = the default workspace of (device, stream), see above.
  * Rejects (LQG_EVALIDATION) m < 1 and k*127*127 >= 2^31 (gemm.cpp:53-57). */
 int lqg_gemm_w4a8(const lqg_weights* w, const int8_t* d_x, int64_t ldx,
                   const float* d_token_scales, uint32_t m, void* d_y, int64_t ldy, int y_dtype,
@@ -204,8 +211,10 @@ int lqg_gemm_w4a8_grouped_accum(const lqg_weights* const* weights, uint32_t num_
 /* Host-buffer call with the reference's convention: x is m*k int8 codes
  * (row-major, ActivationQuant::values, gemm.hpp:35-39), token_scales m floats,
  * y receives m*n values of y_dtype, row-major. Stages through device buffers
- * owned by the handle on `stream` and returns after y is written (like the
- * reference, which returns by value). Not re-entrant per handle. */
+ * taken from a process-wide pool (one staging context per concurrent call)
+ * on `stream` and returns after y is written (like the reference, which
+ * returns by value). Re-entrant: any number of host threads may call it on
+ * the same or different handles (the handle is never modified). */
 int lqg_gemm_w4a8_host(const lqg_weights* w, const int8_t* x, const float* token_scales,
                        uint32_t m, void* y, int y_dtype, void* stream);
 int lqg_gemm_w4a8_accum_host(const lqg_weights* w, const int8_t* x, uint32_t m, int32_t* acc,
@@ -226,6 +235,16 @@ int lqg_quantize_activations(const float* d_x, int64_t ldx, uint32_t m, uint32_t
 /* Number of kernels liblqg.so launched on this process so far (all entry
  * points). The bench reports the delta over its timed region. */
 uint64_t lqg_kernel_launch_count(void);
+
+/* Launch-schedule knobs (tuning and testing hook, process-wide): token-tile
+ * cap "max_bn", CTA pairs "pair" (-1 auto, 0 never, 1 wherever legal),
+ * "pair_min_m", "pair_single_tile", ring split "x_ring_bytes",
+ * "max_x_stages", "max_w_stages", "grid", "raster_gm", "no_dp", "no_pdl".
+ * Results are bit-identical under every setting; only the schedule changes.
+ * Unknown names and out-of-range values -> LQG_EVALIDATION. */
+int lqg_tune_set(const char* name, int64_t value);
+int lqg_tune_get(const char* name, int64_t* value);
+void lqg_tune_reset(void);
 
 const char* lqg_last_error(void);
 const char* lqg_version(void);

@@ -14,14 +14,15 @@ from .lq import (ActivationQuant, CudaError, DeviceWeights, Engine, FragmentDesc
                  IoError, QuantizedWeightBundle, TileConfig, UnsupportedDeviceError,
                  ValidationError, VerificationError, WeightLayout, Workspace, gemm_grouped,
                  gemm_grouped_accum, gemm_w4a8, gemm_w4a8_accum, launch_count, quantize_activations,
-                 quantize_activations_per_token)
+                 quantize_activations_per_token, tune, tune_get, tune_set)
 
 __all__ = [
     "ActivationQuant", "CudaError", "DeviceWeights", "Engine", "FragmentDescriptor", "GemmShape",
     "IoError", "QuantizedWeightBundle", "TileConfig", "UnsupportedDeviceError", "ValidationError",
     "VerificationError", "WeightLayout", "Workspace", "gemm_grouped", "gemm_grouped_accum",
     "gemm_w4a8", "gemm_w4a8_accum",
-    "launch_count", "quantize_activations", "quantize_activations_per_token", "build",
+    "launch_count", "quantize_activations", "quantize_activations_per_token", "tune", "tune_get",
+    "tune_set", "build",
 ]
 
 

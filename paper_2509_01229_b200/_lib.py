@@ -107,6 +107,12 @@ def lib() -> C.CDLL:
             continue
         f.argtypes = args
         f.restype = C.c_int
+    if hasattr(L, "lqg_tune_set"):
+        L.lqg_tune_set.argtypes = [C.c_char_p, i64]
+        L.lqg_tune_set.restype = C.c_int
+        L.lqg_tune_get.argtypes = [C.c_char_p, C.POINTER(i64)]
+        L.lqg_tune_get.restype = C.c_int
+        L.lqg_tune_reset.restype = None
     L.lqg_image_bytes.argtypes = [u32, u32, u32]
     L.lqg_image_bytes.restype = C.c_uint64
     L.lqg_weights_device_bytes.argtypes = [vp]
@@ -127,5 +133,6 @@ EXPORTS = [
     "lqg_workspace_create", "lqg_workspace_destroy", "lqg_gemm_w4a8", "lqg_gemm_w4a8_accum",
     "lqg_gemm_w4a8_grouped", "lqg_gemm_w4a8_grouped_accum", "lqg_gemm_w4a8_fanout",
     "lqg_gemm_w4a8_host", "lqg_gemm_w4a8_accum_host", "lqg_dequant_weights",
-    "lqg_quantize_activations", "lqg_kernel_launch_count", "lqg_last_error", "lqg_version",
+    "lqg_quantize_activations", "lqg_kernel_launch_count", "lqg_tune_set", "lqg_tune_get",
+    "lqg_tune_reset", "lqg_last_error", "lqg_version",
 ]

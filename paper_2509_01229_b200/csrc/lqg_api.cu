@@ -110,32 +110,71 @@ struct lqg_weights {
     uint8_t* d_img = nullptr;
     uint64_t img_bytes = 0;
     float* d_cs = nullptr;
-    lqg_workspace* ws = nullptr;
-    // host-call staging
-    int8_t* d_x = nullptr;
-    size_t x_cap = 0;
-    float* d_ts = nullptr;
-    size_t ts_cap = 0;
-    void* d_y = nullptr;
-    size_t y_cap = 0;
-    // host-call pipeline: copy-in / copy-out streams and per-chunk events
-    cudaStream_t s_in = nullptr, s_out = nullptr;
-    cudaEvent_t ev[2 * 8 + 1] = {};
 };
 
 namespace {
 
+// Runs `f` with this thread's stream-capture mode relaxed, so that the
+// one-off allocations and initialisation below are legal while another
+// stream (e.g. a CUDA-graph capture of the first GEMMs) is capturing.
+template <typename F>
+auto relaxed_capture(F&& f) {
+    cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+    cudaThreadExchangeStreamCaptureMode(&mode);
+    auto r = f();
+    cudaThreadExchangeStreamCaptureMode(&mode);
+    return r;
+}
+
 int workspace_create(int dev, lqg_workspace** out) {
-    auto* w = new lqg_workspace();
-    w->device = dev;
-    DeviceGuard g(dev);
-    if (cudaMalloc(&w->parts, (kMaxSlots * kSlotCells + kMaxSlots) * 4) != cudaSuccess) {
-        delete w;
-        return set_err(LQG_ECUDA, "workspace allocation failed");
-    }
-    fill_i32_kernel<<<592, 256>>>(w->parts, kMaxSlots * kSlotCells, INT32_MIN);
-    fill_i32_kernel<<<1, 256>>>(w->parts + kMaxSlots * kSlotCells, kMaxSlots, 0);
-    if (cudaDeviceSynchronize() != cudaSuccess) return set_err(LQG_ECUDA, "workspace memset failed");
+    return relaxed_capture([&]() -> int {
+        auto* w = new lqg_workspace();
+        w->device = dev;
+        DeviceGuard g(dev);
+        cudaStream_t st = nullptr;
+        if (cudaMalloc(&w->parts, (kMaxSlots * kSlotCells + kMaxSlots) * 4) != cudaSuccess ||
+            cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) {
+            cudaFree(w->parts);
+            delete w;
+            return set_err(LQG_ECUDA, "workspace allocation failed");
+        }
+        fill_i32_kernel<<<592, 256, 0, st>>>(w->parts, kMaxSlots * kSlotCells, INT32_MIN);
+        fill_i32_kernel<<<1, 256, 0, st>>>(w->parts + kMaxSlots * kSlotCells, kMaxSlots, 0);
+        const cudaError_t e = cudaStreamSynchronize(st);
+        cudaStreamDestroy(st);
+        if (e != cudaSuccess) {
+            cudaFree(w->parts);
+            delete w;
+            return set_err(LQG_ECUDA, "workspace initialisation failed");
+        }
+        *out = w;
+        return LQG_OK;
+    });
+}
+
+// The default split-K workspace of a (device, stream): shared by every
+// handle, created on first use and kept for the life of the process. Launches
+// on one stream are ordered, so they can share one workspace; launches on
+// different streams get different ones, which keeps concurrent launches
+// through one (immutable) handle safe without an explicit workspace.
+int default_workspace(int dev, cudaStream_t st, lqg_workspace** out) {
+    struct Entry {
+        int dev;
+        cudaStream_t st;
+        lqg_workspace* ws;
+    };
+    static std::mutex mu;
+    static std::vector<Entry>* pool = new std::vector<Entry>();  // process lifetime
+    std::lock_guard<std::mutex> lk(mu);
+    for (const Entry& e : *pool)
+        if (e.dev == dev && e.st == st) {
+            *out = e.ws;
+            return LQG_OK;
+        }
+    lqg_workspace* w = nullptr;
+    int rc = workspace_create(dev, &w);
+    if (rc) return rc;
+    pool->push_back({dev, st, w});
     *out = w;
     return LQG_OK;
 }
@@ -298,13 +337,6 @@ int alloc_weights(int dev, const ImageGeom& G, lqg_weights** out) {
         delete w;
         return set_err(LQG_ECUDA, "weight image allocation failed");
     }
-    rc = workspace_create(dev, &w->ws);
-    if (rc) {
-        cudaFree(w->d_img);
-        cudaFree(w->d_cs);
-        delete w;
-        return rc;
-    }
     *out = w;
     return LQG_OK;
 }
@@ -312,27 +344,140 @@ int alloc_weights(int dev, const ImageGeom& G, lqg_weights** out) {
 // Token tile: <= 192 so that the INT32 accumulator stays double-buffered in
 // TMEM (2 x 192 columns + a 2-slot A ring, see tmem_plan).
 constexpr uint32_t kMaxTileM = 192;
-// Token tiles up to this size run in decode mode (see launch_gemm).
-constexpr uint32_t kDecodeMaxBN = 32;
+constexpr uint32_t kPairMinM = 320;  // CTA pairs from this many tokens (largest group)
+constexpr uint32_t kDecodeWStages = 6;  // W ring depth for token tiles <= 32
+constexpr uint32_t kMaxGroups = 64;  // experts per grouped launch
+// Dynamic shared memory: the two rings, then barriers / schedule / token scales.
+constexpr uint32_t kSmemMax = 227 * 1024;
+constexpr uint32_t kSmemMisc = 4096;  // 1024-byte alignment pad + barriers + misc (< 3 KB)
 
-constexpr uint32_t kPairMinM = 320;  // auto CTA-pair threshold (tokens)
+// Launch-schedule knobs: token-tile cap, CTA-pair policy, ring split, grid.
+// Results never depend on them (every setting is bit-exact, tested); they
+// only move the schedule. Defaults are the measured best on B200; tools and
+// tests change them through lqg_tune_set (process-wide, no environment reads).
+enum TuneId : int {
+    kTuneMaxBN, kTunePairMinM, kTunePair, kTunePairSingleTile, kTuneXRingBytes, kTuneMaxXStages,
+    kTuneMaxWStages, kTuneGrid, kTuneRasterGM, kTuneNoDP, kTuneNoPDL, kTuneCount
+};
+struct TuneDef {
+    const char* name;
+    int64_t dflt, lo, hi;
+};
+constexpr TuneDef kTuneDefs[kTuneCount] = {
+    {"max_bn", kMaxTileM, 16, kMaxTileM},          // token-tile cap
+    {"pair_min_m", kPairMinM, 1, 1 << 30},         // CTA pairs from this many tokens
+    {"pair", -1, -1, 1},                           // -1 auto, 0 never, 1 wherever legal
+    {"pair_single_tile", 0, 0, 1},                 // allow pairs with one token tile
+    {"x_ring_bytes", 0, 0, kSmemMax},              // 0 = balanced rings; else reserve for X
+    {"max_x_stages", kMaxStages, 2, kMaxStages},
+    {"max_w_stages", kMaxStages, 2, kMaxStages},
+    {"grid", 0, 0, kMaxSlots},                     // 0 = one CTA per SM
+    {"raster_gm", 0, 0, 1 << 20},                  // 0 = derived
+    {"no_dp", 0, 0, 1},                            // stream-K over all tiles
+    {"no_pdl", 0, 0, 1},                           // no programmatic dependent launch
+};
+std::atomic<int64_t> g_tune[kTuneCount] = {
+    {kTuneDefs[0].dflt}, {kTuneDefs[1].dflt}, {kTuneDefs[2].dflt}, {kTuneDefs[3].dflt},
+    {kTuneDefs[4].dflt}, {kTuneDefs[5].dflt}, {kTuneDefs[6].dflt}, {kTuneDefs[7].dflt},
+    {kTuneDefs[8].dflt}, {kTuneDefs[9].dflt}, {kTuneDefs[10].dflt}};
 
-uint32_t env_u32(const char* name, uint32_t dflt) {
-    const char* v = std::getenv(name);
-    return v && *v ? static_cast<uint32_t>(std::strtoul(v, nullptr, 10)) : dflt;
+struct Knobs {
+    uint32_t max_bn, pair_min_m;
+    int pair;
+    uint32_t pair_single_tile, x_ring_bytes, max_x_stages, max_w_stages, grid, raster_gm, no_dp, no_pdl;
+};
+Knobs knobs() {
+    auto g = [](TuneId i) { return g_tune[i].load(std::memory_order_relaxed); };
+    Knobs k;
+    k.max_bn = uint32_t(g(kTuneMaxBN));
+    k.pair_min_m = uint32_t(g(kTunePairMinM));
+    k.pair = int(g(kTunePair));
+    k.pair_single_tile = uint32_t(g(kTunePairSingleTile));
+    k.x_ring_bytes = uint32_t(g(kTuneXRingBytes));
+    k.max_x_stages = uint32_t(g(kTuneMaxXStages));
+    k.max_w_stages = uint32_t(g(kTuneMaxWStages));
+    k.grid = uint32_t(g(kTuneGrid));
+    k.raster_gm = uint32_t(g(kTuneRasterGM));
+    k.no_dp = uint32_t(g(kTuneNoDP));
+    k.no_pdl = uint32_t(g(kTuneNoPDL));
+    return k;
 }
 
-uint32_t choose_bn(uint32_t m, uint32_t* mt) {
-    static const uint32_t cap = env_u32("LQG_DEBUG_MAX_BN", kMaxTileM);
+uint32_t choose_bn(uint32_t m, uint32_t cap, uint32_t* mt) {
     const uint32_t MT = (m + cap - 1) / cap;
     const uint32_t per = (m + MT - 1) / MT;
     *mt = MT;
     return std::max(16u, (per + 15) / 16 * 16);
 }
 
-std::once_flag g_attr_once[64];
+// Activation tensor maps, cached per thread: encoding one costs ~1 us of host
+// time, which matters for eager decode GEMMs of a few microseconds. The key
+// is everything the map encodes.
+struct TmapKey {
+    const void* ptr;
+    uint64_t k, m, ldx;
+    uint32_t box_rows;
+    bool operator==(const TmapKey& o) const {
+        return ptr == o.ptr && k == o.k && m == o.m && ldx == o.ldx && box_rows == o.box_rows;
+    }
+};
 
-constexpr uint32_t kMaxGroups = 64;  // experts per grouped launch
+int activation_tmap(const int8_t* d_x, uint32_t k, uint32_t m, int64_t ldx, uint32_t box_rows, CUtensorMap* out) {
+    constexpr int kCache = 16;
+    struct Entry {
+        TmapKey key;
+        CUtensorMap map;
+        bool used;
+    };
+    static thread_local Entry cache[kCache];
+    static thread_local int next = 0;
+    const TmapKey key{d_x, k, m, uint64_t(ldx), box_rows};
+    for (const Entry& e : cache)
+        if (e.used && e.key == key) {
+            *out = e.map;
+            return LQG_OK;
+        }
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) return set_err(LQG_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t dims[2] = {k, m};
+    const cuuint64_t strides[1] = {cuuint64_t(ldx)};
+    const cuuint32_t box[2] = {kXAtom, box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult cr = enc(out, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(d_x), dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS)
+        return set_err(LQG_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(int(cr)) + ")");
+    Entry& e = cache[next];
+    next = (next + 1) % kCache;
+    e.key = key;
+    e.map = *out;
+    e.used = true;
+    return LQG_OK;
+}
+
+template <uint32_t kG, bool kFan, bool kPair>
+int set_smem_attr() {
+    static const cudaError_t e = cudaFuncSetAttribute(lqg_w4a8_gemm_kernel<kG, kFan, kPair>,
+                                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
+    if (e != cudaSuccess) return set_err(LQG_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+    return LQG_OK;
+}
+
+// Co-resident 2-CTA clusters for the pair kernel at this shared-memory size
+// (not every SM can host half of a cluster: GPC / TPC boundaries), per device.
+int pair_clusters(int device, size_t smem, cudaLaunchConfig_t cfg) {
+    static std::mutex mu;
+    static std::vector<std::pair<std::pair<int, size_t>, int>> memo;
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto& e : memo)
+        if (e.first.first == device && e.first.second == smem) return e.second;
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, lqg_w4a8_gemm_kernel<1, false, true>, &cfg) != cudaSuccess) nc = 0;
+    cudaGetLastError();
+    memo.push_back({{device, smem}, nc});
+    return nc;
+}
 
 // One launch over `ng` weight groups sharing n, k and group size (ng == 1: a
 // plain GEMM). Group e owns rows [row0_e, row0_e + m[e]) of X, token scales
@@ -341,6 +486,7 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
                 const int8_t* d_x, int64_t ldx, const float* d_ts, void* d_out, int64_t ldo,
                 uint32_t out_kind, lqg_workspace* ws, cudaStream_t stream,
                 void* const* fan = nullptr, uint32_t n_fan = 0) {
+    const Knobs K = knobs();
     const lqg_weights* w = ws_list[0];
     const ImageGeom& G = w->geom;
     uint64_t rows = 0;
@@ -364,39 +510,33 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
     if (ldx < int64_t(G.k) || ldx % 16 != 0 || (reinterpret_cast<uintptr_t>(d_x) % 16) != 0)
         return set_err(LQG_EVALIDATION, "activation pitch must be >= k and 16-byte aligned");
     if (ldo < int64_t(G.n)) return set_err(LQG_EVALIDATION, "output pitch must be >= n");
+    if (n_fan > 7) return set_err(LQG_EVALIDATION, "at most 8 output destinations");
+    for (uint32_t r = 0; r < n_fan; ++r)
+        if (!fan[r]) return set_err(LQG_EVALIDATION, "null device pointer");
     if (ws && ws->device != w->device)
         return set_err(LQG_EVALIDATION, "workspace lives on another device");
-    lqg_workspace* W = ws ? ws : w->ws;
-
-    EncodeTiledFn enc = encode_fn();
-    if (!enc) return set_err(LQG_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    lqg_workspace* W = ws;
+    if (!W) {
+        int rc = default_workspace(w->device, stream, &W);
+        if (rc) return rc;
+    }
 
     // Token tile from the largest group; every group gets ceil(m_e / BN) tiles.
     uint32_t MT;
-    uint32_t BN = choose_bn(max_m, &MT);
-    // CTA pairs (tcgen05 cta_group::2) for multi-token-tile plain GEMMs: the
-    // two CTAs of a cluster own adjacent weight tiles and each loads half of
-    // the activation tile, halving the per-SM activation SMEM traffic. The
-    // token tile is a multiple of 32 (16 tokens per CTA half). Default: on from
-    // kPairMinM tokens (LLaMA-2-70B 4-GEMM step on B200: -6 % at M = 320,
-    // -5 % at 1024, -12 % at 8192, but +6 % at 256); LQG_PAIR=0 / 1 forces it
-    // off / on.
-    const uint32_t pair_mode = env_u32("LQG_PAIR", 2);
-    // Grouped launches decide on the largest group (its token tiles dominate).
-    const bool pair = (pair_mode == 1 || (pair_mode == 2 && max_m >= env_u32("LQG_PAIR_MIN_M", kPairMinM))) &&
-                      n_fan == 0 && MT > 1 && G.NT % 2 == 0 && w->num_sms >= 2;
+    uint32_t BN = choose_bn(max_m, K.max_bn, &MT);
+    // CTA pairs (tcgen05 cta_group::2) for multi-token-tile GEMMs: the two
+    // CTAs of a cluster own adjacent weight tiles and each loads half of the
+    // activation tile, halving the per-SM activation SMEM traffic. The token
+    // tile is a multiple of 32 (16 tokens per CTA half). Grouped launches
+    // decide on the largest group (its token tiles dominate).
+    const bool pair_legal = n_fan == 0 && (MT > 1 || K.pair_single_tile) && G.NT % 2 == 0 && w->num_sms >= 2;
+    const bool pair = pair_legal && (K.pair == 1 || (K.pair == -1 && max_m >= K.pair_min_m));
     if (pair) BN = std::min(kMaxTileM, (BN + 31) / 32 * 32);
     CUtensorMap tmap;
-    const cuuint64_t dims[2] = {G.k, m};
-    const cuuint64_t strides[1] = {cuuint64_t(ldx)};
-    const cuuint32_t box[2] = {kXAtom, pair ? BN / 2 : BN};
-    const cuuint32_t estr[2] = {1, 1};
-    CUresult cr = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(d_x), dims,
-                      strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (cr != CUDA_SUCCESS)
-        return set_err(LQG_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(int(cr)) + ")");
+    {
+        int rc = activation_tmap(d_x, G.k, m, ldx, pair ? BN / 2 : BN, &tmap);
+        if (rc) return rc;
+    }
 
     GroupTable<kMaxGroups> gt{};
     uint32_t tiles = 0, row0 = 0;
@@ -417,11 +557,7 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
     p.ts = d_ts;
     p.out = d_out;
     p.ldo = ldo;
-    if (n_fan > 7) return set_err(LQG_EVALIDATION, "at most 8 output destinations");
-    for (uint32_t r = 0; r < n_fan; ++r) {
-        if (!fan[r]) return set_err(LQG_EVALIDATION, "null device pointer");
-        p.fan[r] = fan[r];
-    }
+    for (uint32_t r = 0; r < n_fan; ++r) p.fan[r] = fan[r];
     p.n_fan = n_fan;
     p.parts = W->parts;
     p.flags = reinterpret_cast<uint32_t*>(W->parts + kMaxSlots * kSlotCells);
@@ -435,85 +571,62 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
     p.P = G.P;
     p.chunk_bytes = G.chunk_bytes;
     p.out_kind = out_kind;
-    p.stage_bytes = ((pair ? BN / 2 : BN) * kKBlock + G.chunk_bytes + 1023) / 1024 * 1024;
-    // Co-resident mode (opt-in, LQG_CORESIDENT=1, single group, small token
-    // tiles): <= 110 KB of shared memory, 256 TMEM columns and one dequant
-    // warpgroup so that two CTAs fit on an SM and the next GEMM's CTAs are
-    // resident while this one drains. Measured on B200 it loses to one CTA per
-    // SM with the full 227 KB ring (LLaMA-2-70B 4-layer step at M = 16: 95 vs
-    // 81 us): the halved ring slows the mainloop more than the earlier start gains.
-    const bool decode = ng == 1 && n_fan == 0 && BN <= kDecodeMaxBN && env_u32("LQG_CORESIDENT", 0);
-    p.tmem_cols = decode ? 256 : 512;
-    // ~24 MB of weights across the grid (enough to cover a kernel tail at HBM rate).
-    p.l2_prefetch = env_u32("LQG_L2_PREFETCH_CHUNKS", decode ? 4 : 0);
-    p.w_split = std::max(1u, env_u32("LQG_DEBUG_WSPLIT", 1));
-    p.l2_last = env_u32("LQG_L2_EVICT_LAST", 1);
-    p.pdl_trigger = env_u32("LQG_PDL_TRIGGER", decode ? 2 : 0);
     p.trace_slot = static_cast<uint32_t>(g_launches.load(std::memory_order_relaxed) % 8);
-    const uint32_t budget = decode ? 110 * 1024 - 5120 : 227 * 1024 - 5120;
-    p.stages = std::min<uint32_t>(kMaxStages, budget / p.stage_bytes);
-    if (uint32_t st = env_u32("LQG_DEBUG_STAGES", 0)) p.stages = std::min(p.stages, st);
-    if (p.stages < 2) return set_err(LQG_EVALIDATION, "tile configuration does not fit shared memory");
-    if (tmem_plan(BN, p.tmem_cols).a_slots < 1)
+    // Rings. The TMA engine serves an SM's copies in issue order, so an
+    // activation tile issued behind d weight chunks lands only after them:
+    // the X ring must run at least as far ahead as the W ring or the MMA
+    // stalls on activations (measured: W 12 deep / X 8 deep at decode, W 8 /
+    // X 2 at M = 128). Both rings get the same depth (W even: the dequant
+    // warpgroups alternate), X takes any remaining space.
+    p.x_slot_bytes = (pair ? BN / 2 : BN) * kKBlock;
+    const uint32_t ring_budget = kSmemMax - kSmemMisc;
+    // Decode tiles (<= 32 tokens) keep the W ring at 6: deeper weight
+    // prefetch only delays the activation tiles queued behind it (LLaMA-2-70B
+    // 4-GEMM step at M = 16: 69 us at 6, 73 us at 10).
+    const uint32_t w_cap = BN <= 32 ? kDecodeWStages : kMaxStages;
+    uint32_t sw = std::min({ring_budget / (p.x_slot_bytes + G.chunk_bytes), K.max_w_stages, w_cap}) & ~1u;
+    if (K.x_ring_bytes) sw = std::min(sw, std::max(2u, ((ring_budget - std::min(ring_budget, K.x_ring_bytes)) / G.chunk_bytes) & ~1u));
+    p.x_stages = std::min({(ring_budget - sw * G.chunk_bytes) / p.x_slot_bytes, K.max_x_stages, kMaxStages});
+    if (p.x_stages < 2) return set_err(LQG_EVALIDATION, "tile configuration does not fit shared memory");
+    p.w_base = p.x_stages * p.x_slot_bytes;
+    // A split-K finisher of a large token tile gathers each contributor's
+    // whole INT32 partial (BN x 128 x 4 bytes) into the idle rings: they must
+    // hold at least one (max_w_stages yields to this).
+    if (BN / 16 > kSentinelMaxChunks) {
+        const uint32_t need = BN * kTileN * 4;
+        while (p.w_base + sw * G.chunk_bytes < need && sw + 2 <= kMaxStages) sw += 2;
+        if (p.w_base + sw * G.chunk_bytes < need || p.w_base + sw * G.chunk_bytes > ring_budget)
+            return set_err(LQG_EVALIDATION, "tile configuration does not fit shared memory");
+    }
+    if (sw < 2) return set_err(LQG_EVALIDATION, "tile configuration does not fit shared memory");
+    p.w_stages = sw;
+    if (tmem_plan(BN).a_slots < 2)
         return set_err(LQG_EVALIDATION, "tile configuration does not fit tensor memory");
-    p.total_iters = uint64_t(tiles) * G.KB;
-    if (p.total_iters * kMaxSlots >= (uint64_t(1) << 32))
+    const uint64_t total_iters = uint64_t(tiles) * G.KB;
+    if (total_iters * kMaxSlots >= (uint64_t(1) << 32))
         return set_err(LQG_EVALIDATION, "problem too large for one launch (tiles x k-blocks x " +
                                             std::to_string(kMaxSlots) + " >= 2^32)");
     uint32_t grid = static_cast<uint32_t>(
-        std::min<uint64_t>(std::min<uint32_t>(w->num_sms, kMaxSlots), p.total_iters));
-    if (uint32_t gd = env_u32("LQG_DEBUG_GRID", 0))
-        grid = static_cast<uint32_t>(std::min<uint64_t>({gd, uint64_t(kMaxSlots), p.total_iters}));
+        std::min<uint64_t>(std::min<uint32_t>(w->num_sms, kMaxSlots), total_iters));
+    if (K.grid) grid = static_cast<uint32_t>(std::min<uint64_t>({K.grid, uint64_t(kMaxSlots), total_iters}));
     // pair mode: scheduling units are CTA pairs (grid = 2 x units)
-    const uint32_t units = pair ? std::max(1u, grid / 2) : grid;
-    if (pair) grid = 2 * units;
-    // Hybrid schedule: whole-tile rounds first, stream-K over the last G..2G
-    // tiles (all tiles when there are fewer than G), tiles rasterized in groups
-    // of GM token tiles sized so that the activation and weight slices of one
-    // round balance in L2 (GM^2 ~ G * weight bytes per tile / activation bytes).
-    {
-        const uint64_t T = tiles;
-        uint32_t dp = 0;
-        if (!decode && T >= units && !env_u32("LQG_DEBUG_NO_DP", 0))
-            dp = static_cast<uint32_t>(T % units == 0 ? T / units : T / units - 1);
-        p.dp_rounds = dp;
-        const double ratio = double(units) * ((pair ? 2 : 1) * kTileN / 2.0) / double(BN);
-        uint32_t gm = static_cast<uint32_t>(std::lround(std::sqrt(ratio)));
-        if (uint32_t e = env_u32("LQG_DEBUG_RASTER_GM", 0)) gm = e;
-        p.raster_gm = std::max(1u, std::min(gm, MT));
-    }
-    const size_t smem = size_t(p.stages) * p.stage_bytes + 1024 + 4096;  // ring + align + barriers/misc
+    uint32_t units = pair ? std::max(1u, grid / 2) : grid;
+    const size_t smem = size_t(p.w_base) + size_t(p.w_stages) * G.chunk_bytes + kSmemMisc;
 
     DeviceGuard dg(w->device);
-    cudaError_t e = cudaSuccess;
-    std::call_once(g_attr_once[w->device % 64], [&] {
-        e = cudaFuncSetAttribute(lqg_w4a8_gemm_kernel<true, 1, false>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(lqg_w4a8_gemm_kernel<false, 1, false>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(lqg_w4a8_gemm_kernel<false, 1, true>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(lqg_w4a8_gemm_kernel<false, kMaxGroups, false>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(lqg_w4a8_gemm_kernel<false, 1, false, true>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(lqg_w4a8_gemm_kernel<false, kMaxGroups, false, true>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    });
-    if (e != cudaSuccess) return set_err(LQG_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+    {
+        int rc = ng > 1 ? (pair ? set_smem_attr<kMaxGroups, false, true>() : set_smem_attr<kMaxGroups, false, false>())
+                        : (pair ? set_smem_attr<1, false, true>()
+                                : (n_fan ? set_smem_attr<1, true, false>() : set_smem_attr<1, false, false>()));
+        if (rc) return rc;
+    }
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(decode ? Roles<true>::kThreadsT : Roles<false>::kThreadsT);
+    cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = env_u32("LQG_DEBUG_NO_PDL", 0) ? 0 : 1;
+    attr[0].val.programmaticStreamSerializationAllowed = K.no_pdl ? 0 : 1;
     attr[1].id = cudaLaunchAttributeClusterDimension;
     attr[1].val.clusterDim.x = pair ? 2 : 1;
     attr[1].val.clusterDim.y = 1;
@@ -521,45 +634,43 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
     cfg.attrs = attr;
     cfg.numAttrs = pair ? 2 : 1;
     if (pair) {
-        // Not every SM can host half of a 2-CTA cluster (GPC / TPC boundaries):
         // size the persistent grid to the clusters that are co-resident, so no
-        // pair runs in a second wave.
-        static thread_local size_t cached_smem = 0;
-        static thread_local int cached_clusters = 0;
-        if (cached_smem != smem) {
-            int nc = 0;
-            if (cudaOccupancyMaxActiveClusters(&nc, lqg_w4a8_gemm_kernel<false, 1, false, true>, &cfg) != cudaSuccess)
-                nc = 0;
-            cudaGetLastError();
-            cached_smem = smem;
-            cached_clusters = nc;
-        }
-        if (cached_clusters > 0 && uint32_t(cached_clusters) < grid / 2) {
-            // re-derive the schedule for fewer pairs
-            const uint32_t u = uint32_t(cached_clusters);
-            cfg.gridDim = dim3(2 * u);
-            const uint64_t T = tiles;
-            p.dp_rounds = (T >= u && !env_u32("LQG_DEBUG_NO_DP", 0))
-                              ? static_cast<uint32_t>(T % u == 0 ? T / u : T / u - 1) : 0;
-        }
+        // pair runs in a second wave
+        cfg.gridDim = dim3(2 * units);
+        const int nc = pair_clusters(w->device, smem, cfg);
+        if (nc > 0 && uint32_t(nc) < units) units = uint32_t(nc);
+        grid = 2 * units;
+    }
+    cfg.gridDim = dim3(grid);
+    // Hybrid schedule: whole-tile rounds first, stream-K over the last G..2G
+    // tiles (all tiles when there are fewer than G), tiles rasterized in groups
+    // of GM token tiles sized so that the activation and weight slices of one
+    // round balance in L2 (GM^2 ~ G * weight bytes per tile / activation bytes).
+    {
+        const uint64_t T = tiles;
+        uint32_t dp = 0;
+        if (T >= units && !K.no_dp) dp = static_cast<uint32_t>(T % units == 0 ? T / units : T / units - 1);
+        p.dp_rounds = dp;
+        const double ratio = double(units) * ((pair ? 2 : 1) * kTileN / 2.0) / double(BN);
+        uint32_t gm = static_cast<uint32_t>(std::lround(std::sqrt(ratio)));
+        if (K.raster_gm) gm = K.raster_gm;
+        p.raster_gm = std::max(1u, std::min(gm, MT));
     }
     if (ng > 1) {
         if (pair)
-            LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<false, kMaxGroups, false, true>, tmap, p, gt));
+            LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<kMaxGroups, false, true>, tmap, p, gt));
         else
-            LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<false, kMaxGroups, false>, tmap, p, gt));
+            LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<kMaxGroups, false, false>, tmap, p, gt));
     } else {
         GroupTable<1> g1{};
         g1.e[0] = gt.e[0];
         g1.n = 1;
         if (pair)
-            LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<false, 1, false, true>, tmap, p, g1));
+            LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<1, false, true>, tmap, p, g1));
         else if (n_fan)
-            LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<false, 1, true>, tmap, p, g1));
-        else if (decode)
-            LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<true, 1, false>, tmap, p, g1));
+            LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<1, true, false>, tmap, p, g1));
         else
-            LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<false, 1, false>, tmap, p, g1));
+            LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<1, false, false>, tmap, p, g1));
     }
     g_launches.fetch_add(1, std::memory_order_relaxed);
     LQG_CUDA(cudaGetLastError());
@@ -610,6 +721,32 @@ int lqg_debug_trace(unsigned long long* out) {
 #endif
 const char* lqg_version(void) { return "lqg 0.1 (sm_100a, tcgen05 kind::i8, TMEM-A LiquidQuant mainloop)"; }
 uint64_t lqg_kernel_launch_count(void) { return g_launches.load(); }
+
+int lqg_tune_set(const char* name, int64_t value) {
+    if (!name) return set_err(LQG_EVALIDATION, "null argument");
+    for (int i = 0; i < kTuneCount; ++i)
+        if (std::strcmp(name, kTuneDefs[i].name) == 0) {
+            if (value < kTuneDefs[i].lo || value > kTuneDefs[i].hi)
+                return set_err(LQG_EVALIDATION, std::string("tune value out of range for ") + name);
+            g_tune[i].store(value, std::memory_order_relaxed);
+            return LQG_OK;
+        }
+    return set_err(LQG_EVALIDATION, std::string("unknown tune knob ") + name);
+}
+
+int lqg_tune_get(const char* name, int64_t* value) {
+    if (!name || !value) return set_err(LQG_EVALIDATION, "null argument");
+    for (int i = 0; i < kTuneCount; ++i)
+        if (std::strcmp(name, kTuneDefs[i].name) == 0) {
+            *value = g_tune[i].load(std::memory_order_relaxed);
+            return LQG_OK;
+        }
+    return set_err(LQG_EVALIDATION, std::string("unknown tune knob ") + name);
+}
+
+void lqg_tune_reset(void) {
+    for (int i = 0; i < kTuneCount; ++i) g_tune[i].store(kTuneDefs[i].dflt, std::memory_order_relaxed);
+}
 
 int lqg_bundle_validate(const lqg_bundle_view* bundle) {
     if (!bundle) return set_err(LQG_EVALIDATION, "null argument");
@@ -789,14 +926,6 @@ int lqg_weights_destroy(lqg_weights* w) {
     DeviceGuard g(w->device);
     cudaFree(w->d_img);
     cudaFree(w->d_cs);
-    cudaFree(w->d_x);
-    cudaFree(w->d_ts);
-    cudaFree(w->d_y);
-    if (w->s_in) cudaStreamDestroy(w->s_in);
-    if (w->s_out) cudaStreamDestroy(w->s_out);
-    for (cudaEvent_t e : w->ev)
-        if (e) cudaEventDestroy(e);
-    lqg_workspace_destroy(w->ws);
     delete w;
     return LQG_OK;
 }
@@ -1079,18 +1208,55 @@ int lqg_gemm_w4a8_accum(const lqg_weights* w, const int8_t* d_x, int64_t ldx, ui
                        static_cast<cudaStream_t>(stream));
 }
 
-static int host_call(const lqg_weights* wc, const int8_t* x, const float* ts, uint32_t m, void* y,
-                     uint32_t kind, size_t ebytes, cudaStream_t st) {
-    auto* w = const_cast<lqg_weights*>(wc);
-    if (!w) return set_err(LQG_EVALIDATION, "null handle");
-    if (m < 1) return set_err(LQG_EVALIDATION, "activation dimensions must be >= 1");
-    if (!x || !y || (kind != kOutAcc && !ts)) return set_err(LQG_EVALIDATION, "null host pointer");
+namespace {
+
+// Device staging of one host-buffer call: X / token-scale / Y buffers, the
+// copy-in and copy-out streams and the per-chunk events. Staging contexts live
+// in a process-wide pool; each call holds one exclusively, so concurrent host
+// threads (on one handle or several) never share buffers, and the weight
+// handle itself stays immutable.
+struct Staging {
+    int device = -1;
+    bool busy = false;
+    int8_t* d_x = nullptr;
+    size_t x_cap = 0;
+    float* d_ts = nullptr;
+    size_t ts_cap = 0;
+    void* d_y = nullptr;
+    size_t y_cap = 0;
+    cudaStream_t s_in = nullptr, s_out = nullptr;
+    cudaEvent_t ev[2 * 8 + 1] = {};
+};
+
+std::mutex g_staging_mu;
+std::vector<Staging*>* g_staging = new std::vector<Staging*>();  // process lifetime
+
+Staging* staging_acquire(int device) {
+    std::lock_guard<std::mutex> lk(g_staging_mu);
+    for (Staging* s : *g_staging)
+        if (!s->busy && s->device == device) {
+            s->busy = true;
+            return s;
+        }
+    auto* s = new Staging();
+    s->device = device;
+    s->busy = true;
+    g_staging->push_back(s);
+    return s;
+}
+
+void staging_release(Staging* s) {
+    std::lock_guard<std::mutex> lk(g_staging_mu);
+    s->busy = false;
+}
+
+int host_call_on(const lqg_weights* w, Staging& S, const int8_t* x, const float* ts, uint32_t m, void* y,
+                 uint32_t kind, size_t ebytes, cudaStream_t st) {
     const ImageGeom& G = w->geom;
-    DeviceGuard g(w->device);
     const int64_t ldx = (int64_t(G.k) + 15) / 16 * 16;
-    int rc = ensure_cap(reinterpret_cast<void**>(&w->d_x), &w->x_cap, size_t(m) * ldx);
-    if (!rc) rc = ensure_cap(reinterpret_cast<void**>(&w->d_ts), &w->ts_cap, size_t(m) * 4);
-    if (!rc) rc = ensure_cap(&w->d_y, &w->y_cap, size_t(m) * G.n * ebytes);
+    int rc = ensure_cap(reinterpret_cast<void**>(&S.d_x), &S.x_cap, size_t(m) * ldx);
+    if (!rc) rc = ensure_cap(reinterpret_cast<void**>(&S.d_ts), &S.ts_cap, size_t(m) * 4);
+    if (!rc) rc = ensure_cap(&S.d_y, &S.y_cap, size_t(m) * G.n * ebytes);
     if (rc) return rc;
     // Large calls are cut into row chunks pipelined over three streams:
     // H2D of chunk c+1 and D2H of chunk c-1 (PCIe is full duplex) overlap the
@@ -1098,21 +1264,21 @@ static int host_call(const lqg_weights* wc, const int8_t* x, const float* ts, ui
     // plus the GEMM. Small calls (latency-bound) stay one chunk.
     const uint32_t per = m >= 2048 ? std::max<uint32_t>(1024, (m + 7) / 8) : m;
     const uint32_t nchunk = (m + per - 1) / per;
-    if (nchunk > 1 && !w->s_in) {
-        LQG_CUDA(cudaStreamCreateWithFlags(&w->s_in, cudaStreamNonBlocking));
-        LQG_CUDA(cudaStreamCreateWithFlags(&w->s_out, cudaStreamNonBlocking));
-        for (cudaEvent_t& e : w->ev) LQG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    if (nchunk > 1 && !S.s_in) {
+        LQG_CUDA(cudaStreamCreateWithFlags(&S.s_in, cudaStreamNonBlocking));
+        LQG_CUDA(cudaStreamCreateWithFlags(&S.s_out, cudaStreamNonBlocking));
+        for (cudaEvent_t& e : S.ev) LQG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
-    cudaStream_t s_in = nchunk > 1 ? w->s_in : st, s_out = nchunk > 1 ? w->s_out : st;
+    cudaStream_t s_in = nchunk > 1 ? S.s_in : st, s_out = nchunk > 1 ? S.s_out : st;
     if (nchunk > 1) {  // the copies start after the caller's prior work on st
-        LQG_CUDA(cudaEventRecord(w->ev[16], st));
-        LQG_CUDA(cudaStreamWaitEvent(s_in, w->ev[16], 0));
-        LQG_CUDA(cudaStreamWaitEvent(s_out, w->ev[16], 0));
+        LQG_CUDA(cudaEventRecord(S.ev[16], st));
+        LQG_CUDA(cudaStreamWaitEvent(s_in, S.ev[16], 0));
+        LQG_CUDA(cudaStreamWaitEvent(s_out, S.ev[16], 0));
     }
     const size_t yrow = size_t(G.n) * ebytes;
     for (uint32_t c = 0; c < nchunk; ++c) {
         const uint32_t r0 = c * per, rows = std::min(per, m - r0);
-        int8_t* dx = w->d_x + size_t(r0) * ldx;
+        int8_t* dx = S.d_x + size_t(r0) * ldx;
         if (ldx == int64_t(G.k)) {
             LQG_CUDA(cudaMemcpyAsync(dx, x + size_t(r0) * G.k, size_t(rows) * G.k, cudaMemcpyHostToDevice, s_in));
         } else {
@@ -1120,25 +1286,41 @@ static int host_call(const lqg_weights* wc, const int8_t* x, const float* ts, ui
                                        cudaMemcpyHostToDevice, s_in));
         }
         if (kind != kOutAcc)
-            LQG_CUDA(cudaMemcpyAsync(w->d_ts + r0, ts + r0, size_t(rows) * 4, cudaMemcpyHostToDevice, s_in));
+            LQG_CUDA(cudaMemcpyAsync(S.d_ts + r0, ts + r0, size_t(rows) * 4, cudaMemcpyHostToDevice, s_in));
         if (nchunk > 1) {
-            LQG_CUDA(cudaEventRecord(w->ev[2 * (c % 8)], s_in));
-            LQG_CUDA(cudaStreamWaitEvent(st, w->ev[2 * (c % 8)], 0));
+            LQG_CUDA(cudaEventRecord(S.ev[2 * (c % 8)], s_in));
+            LQG_CUDA(cudaStreamWaitEvent(st, S.ev[2 * (c % 8)], 0));
         }
-        rc = launch_gemm(w, dx, ldx, w->d_ts + r0, rows, static_cast<uint8_t*>(w->d_y) + r0 * yrow, G.n,
+        rc = launch_gemm(w, dx, ldx, S.d_ts + r0, rows, static_cast<uint8_t*>(S.d_y) + r0 * yrow, G.n,
                          kind, nullptr, st);
         if (rc) return rc;
         if (nchunk > 1) {
-            LQG_CUDA(cudaEventRecord(w->ev[2 * (c % 8) + 1], st));
-            LQG_CUDA(cudaStreamWaitEvent(s_out, w->ev[2 * (c % 8) + 1], 0));
+            LQG_CUDA(cudaEventRecord(S.ev[2 * (c % 8) + 1], st));
+            LQG_CUDA(cudaStreamWaitEvent(s_out, S.ev[2 * (c % 8) + 1], 0));
         }
         LQG_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(y) + r0 * yrow,
-                                 static_cast<uint8_t*>(w->d_y) + r0 * yrow, rows * yrow,
+                                 static_cast<uint8_t*>(S.d_y) + r0 * yrow, rows * yrow,
                                  cudaMemcpyDeviceToHost, s_out));
     }
     LQG_CUDA(cudaStreamSynchronize(s_out));
     if (nchunk > 1) LQG_CUDA(cudaStreamSynchronize(st));
     return LQG_OK;
+}
+
+}  // namespace
+
+// Synchronous host-buffer call (the reference's calling convention).
+// Re-entrant: each call holds its own staging context from the pool.
+static int host_call(const lqg_weights* w, const int8_t* x, const float* ts, uint32_t m, void* y,
+                     uint32_t kind, size_t ebytes, cudaStream_t st) {
+    if (!w) return set_err(LQG_EVALIDATION, "null handle");
+    if (m < 1) return set_err(LQG_EVALIDATION, "activation dimensions must be >= 1");
+    if (!x || !y || (kind != kOutAcc && !ts)) return set_err(LQG_EVALIDATION, "null host pointer");
+    DeviceGuard g(w->device);
+    Staging* S = staging_acquire(w->device);
+    const int rc = host_call_on(w, *S, x, ts, m, y, kind, ebytes, st);
+    staging_release(S);
+    return rc;
 }
 
 int lqg_gemm_w4a8_host(const lqg_weights* w, const int8_t* x, const float* ts, uint32_t m, void* y,

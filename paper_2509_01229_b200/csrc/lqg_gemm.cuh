@@ -8,36 +8,45 @@
 // Hardware mapping (swap-AB: the tcgen05 M dimension is the weight row):
 //   D[128 rows x BN tokens] (INT32, TMEM) += A[128 x 32] (int8, TMEM) * B[32 x BN] (int8, SMEM)
 //
-// Warp roles in one 512-thread CTA (one CTA per SM, persistent, stream-K):
-//   warp 0        TMA producer: per 256-wide k-block, one 1-D bulk copy of
-//                 the prepacked weight chunk (codes + group params,
-//                 EVICT_FIRST) and two 2-D SW128 tensor copies of the
-//                 activation tile (EVICT_LAST) into an S-stage SMEM ring.
-//   warp 1        MMA issuer: 8 x tcgen05.mma.kind::i8 (K=32 each) per
-//                 k-block, A read from TMEM, B from the swizzled ring slot;
-//                 tcgen05.commit frees the ring slot and the TMEM A slot and
-//                 signals the epilogue at the end of a tile segment.
-//   warp 2        TMEM allocator (512 columns).
-//   warps 4-11    two dequant warpgroups (ImFP), each taking half
-//                 of every k-block: LDS.128 of packed codes, LiquidQuant
-//                 (q*s + a) ^ 0x80 on four byte lanes per IMAD
-//                 (packed.cpp:40-61), tcgen05.st of the INT8
-//                 result into the TMEM A ring (thread = weight row = lane).
-//   warps 12-15   epilogue: tcgen05.ld of the INT32 accumulators, fused
+// Warp roles in one 480-thread CTA (one CTA per SM, persistent, stream-K):
+//   warp 0        W producer: per 256-wide k-block one 1-D bulk copy of the
+//                 prepacked weight chunk (codes + group params) into the
+//                 W ring. The first ring of chunks is requested before
+//                 griddepcontrol.wait (weights do not depend on the
+//                 previous kernel).
+//   warp 14       X producer: two 2-D SW128 tensor copies of the activation
+//                 tile per k-block into the X ring (after griddepcontrol.wait).
+//   warp 1        MMA issuer (+ TMEM allocation, 512 columns): 8 x
+//                 tcgen05.mma.kind::i8 (K = 32 each) per k-block, A from
+//                 TMEM, B from the X ring; tcgen05.commit frees the X slot
+//                 and the TMEM A slot and signals the epilogue at the end of
+//                 a tile segment.
+//   warps 2-9     two dequant warpgroups (the paper's ImFP compute WGs,
+//                 P:415-416) taking alternate k-blocks: LDS of the packed
+//                 codes and group parameters (one 2..16-byte LDS per k-block
+//                 for the parameters), W slot released as soon as the codes
+//                 are in registers, LiquidQuant (q*s + a) ^ 0x80 on four byte
+//                 lanes per IMAD (packed.cpp:40-61), tcgen05.st of
+//                 the INT8 result into the TMEM A ring (thread = weight row =
+//                 TMEM lane).
+//   warps 10-13   epilogue: tcgen05.ld of the INT32 accumulators, fused
 //                 per-channel x per-token scaling and F32/F16/BF16 cast,
-//                 coalesced stores (or the INT32 accumulators themselves).
-// All hand-offs are mbarrier arrivals (TMA complete_tx, tcgen05.commit,
-// thread arrives); there is no __syncthreads in the mainloop.
+//                 stores (or the INT32 accumulators themselves), split-K
+//                 exchange.
+// The W ring (freed by the dequant warps) and the X ring (freed by the MMA)
+// are separate, so a weight chunk's SMEM slot turns over after load latency +
+// dequant only, and the weight stream keeps many chunks in flight whatever
+// the token tile. All hand-offs are mbarrier arrivals (TMA complete_tx,
+// tcgen05.commit, thread arrives); there is no __syncthreads in the mainloop.
 //
 // TMEM (512 columns): [0, acc_stages*acc_stride) INT32 accumulators, then
 // the A ring of a_slots x 64 columns (one 256-wide k-block of int8 per slot).
 //
-// Stream-K: the linear space of (tile, k-block) iterations is cut into
-// gridDim.x contiguous ranges. A tile whose k-range is split between CTAs is
-// reduced exactly in INT32 (red.global.add into a per-launch workspace slot,
-// then the CTA that completes the tile's k-count applies the epilogue and
-// re-zeroes the slot). Integer addition is associative, so the result is
-// bit-identical to the reference's fixed-order sum.
+// Work split: whole-tile rounds, then stream-K over the remaining tiles'
+// (tile, k-block) space. A tile whose k-range spans several CTAs is reduced
+// exactly in INT32 through a workspace (see the epilogue); integer addition
+// is associative, so results are bit-identical to the reference's fixed-order
+// sum in any arrival order.
 #pragma once
 #include <cstdint>
 #include <cuda.h>
@@ -51,21 +60,14 @@ namespace lqg {
 
 enum OutKind : uint32_t { kOutAcc = 0, kOutF32 = 1, kOutF16 = 2, kOutBF16 = 3 };
 
-// Warp roles: 0 TMA producer, 1 MMA issuer (+ TMEM alloc), then the dequant
-// warpgroups, then 4 epilogue warps. One CTA per SM: two dequant WGs (448
-// threads). Co-resident decode mode (two CTAs per SM): one dequant WG (320
-// threads, so each CTA keeps ~100 registers per thread) -- at BN <= 32 one WG
-// dequantizes a k-block several times faster than HBM delivers it.
-constexpr uint32_t kThreads = 448;
-constexpr uint32_t kDequantWarp0 = 2;
-constexpr uint32_t kEpiWarp0 = 10;
-template <bool kDecode>
-struct Roles {
-    static constexpr uint32_t kDQWarps = kDecode ? 4 : 8;
-    static constexpr uint32_t kEpi0 = kDequantWarp0 + kDQWarps;
-    static constexpr uint32_t kThreadsT = (kEpi0 + 4) * 32;
-};
-constexpr uint32_t kMaxStages = 16;
+constexpr uint32_t kWarpW = 0;         // weight producer
+constexpr uint32_t kWarpMMA = 1;       // MMA issuer, TMEM allocator
+constexpr uint32_t kDequantWarp0 = 2;  // two warpgroups: warps 2-5, 6-9
+constexpr uint32_t kDQWarps = 8;
+constexpr uint32_t kEpiWarp0 = 10;     // warps 10-13
+constexpr uint32_t kWarpX = 14;        // activation producer
+constexpr uint32_t kThreads = 15 * 32;
+constexpr uint32_t kMaxStages = 16;    // per ring
 constexpr uint32_t kMaxASlots = 8;
 constexpr uint32_t kACols = kKBlock / 4;   // TMEM columns per A slot (4 int8 per column)
 constexpr uint32_t kMaxBN = 256;
@@ -82,15 +84,19 @@ struct TmemPlan {
     uint32_t acc_stride, acc_stages, a_base, a_slots;
 };
 
-// cols = allocated TMEM columns: 512 (one CTA per SM) or 256 (decode mode:
-// two co-resident CTAs, e.g. consecutive GEMMs overlapped by PDL).
-__host__ __device__ inline TmemPlan tmem_plan(uint32_t BN, uint32_t cols) {
+// 512 TMEM columns: double-buffered accumulators whenever two fit next to an
+// A ring of >= 2 slots; the A ring is even (the two dequant warpgroups take
+// alternate k-blocks, so each waits on every other slot and must see every
+// phase of its slots).
+__host__ __device__ inline TmemPlan tmem_plan(uint32_t BN) {
+    constexpr uint32_t cols = 512;
     TmemPlan t;
     t.acc_stride = (BN + 31) / 32 * 32;
     t.acc_stages = (2 * t.acc_stride + 2 * kACols <= cols) ? 2u : 1u;
     t.a_base = (t.acc_stages * t.acc_stride + kACols - 1) / kACols * kACols;
     t.a_slots = (cols - t.a_base) / kACols;
     if (t.a_slots > kMaxASlots) t.a_slots = kMaxASlots;
+    t.a_slots &= ~1u;
     return t;
 }
 
@@ -100,29 +106,24 @@ struct GemmParams {
     int64_t ldo;               // row pitch of out (and of every fan-out copy), in elements
     void* fan[7];              // extra destinations receiving the same tile (e.g. peer GPUs'
     uint32_t n_fan;            //   Y over NVLink: the fused all-gather of the N-split driver)
-    int32_t* parts;            // split-K partials: per CTA kMaxBN*128 int32 cells,
-                               // [chunk][quad][row] int4
+    int32_t* parts;            // split-K partials: per CTA kSlotCellsK int32 cells
     uint32_t* flags;           // per CTA: 1 = partial published (release), reset by the finisher
     uint32_t N;                // weight rows
     uint32_t KB, NT, MT;       // k-blocks, weight tiles, token tiles (of the largest group)
     uint32_t BN;               // tokens per tile (16..256, multiple of 16)
     uint32_t P;                // group params per k-block (1, 2, 4, 8)
     uint32_t chunk_bytes;      // bytes per (tile, k-block) weight chunk
-    uint32_t stages;           // shared-memory ring depth
-    uint32_t stage_bytes;      // bytes per ring slot (X tile first, then W chunk)
     uint32_t out_kind;         // OutKind
-    uint32_t tmem_cols;        // 256 (decode mode) or 512
-    uint32_t l2_prefetch;      // weight chunks prefetched into L2 ahead of the SMEM ring
-    uint32_t w_split;          // bulk copies per weight chunk (1, 2, 4)
+    uint32_t x_stages;         // X ring depth
+    uint32_t x_slot_bytes;     // bytes per X slot (this CTA's share of the activation tile)
+    uint32_t w_stages;         // W ring depth (even)
+    uint32_t w_base;           // byte offset of the W ring (after the X ring)
     uint32_t dp_rounds;        // whole tiles per CTA before the stream-K tail
     uint32_t raster_gm;        // token tiles per raster group
     uint32_t trace_slot;       // LQG_TRACE builds: launch index % 8
-    uint32_t l2_last;          // 1: EVICT_LAST cache hints for reused tiles (default)
     uint32_t pair;             // 1: CTA pairs (cluster of 2, tcgen05 cta_group::2, M = 256):
                                //    NT/tiles count pair tiles, each CTA owns weight tile 2*nt+rank
                                //    and loads half of every activation tile
-    uint32_t pdl_trigger;
-    uint64_t total_iters;      // tiles*KB
     uint32_t tiles;            // weight-tile x token-tile pairs (summed over groups)
 };
 
@@ -193,11 +194,11 @@ __device__ __forceinline__ uint32_t range_begin32(uint32_t c, uint32_t G, uint32
     return static_cast<uint32_t>((uint64_t(total) * c) / G);
 }
 
-// Computed once per CTA (thread 0) and shared through SMEM.
 // Scheduling units: CTAs, or CTA pairs (p.pair).
 __device__ __forceinline__ uint32_t sched_units(const GemmParams& p) {
     return p.pair ? gridDim.x >> 1 : gridDim.x;
 }
+// Computed once per CTA (thread 0) and shared through SMEM.
 __device__ __forceinline__ Sched make_sched(const GemmParams& p) {
     Sched s;
     const uint32_t G = sched_units(p);
@@ -216,15 +217,13 @@ __device__ __forceinline__ Sched make_sched(const GemmParams& p) {
 // Position in one CTA's iteration sequence (DP tiles, then its stream-K range).
 // Self-contained (KB / dp_rounds come from the kernel parameter bank) so that
 // no per-CTA schedule state stays live across the role loops.
-// kDP = false (decode mode: dp_rounds == 0) drops the data-parallel phase.
-template <bool kDP>
 struct Walk {
     uint32_t tile, kb, r, sk_tile, sk_kb;
     __device__ __forceinline__ void init(const Sched& s) {
         r = 0;
         sk_tile = s.sk_tile;
         sk_kb = s.sk_kb;
-        if (kDP && s.dp_rounds > 0) {
+        if (s.dp_rounds > 0) {
             tile = s.c;
             kb = 0;
         } else {
@@ -236,7 +235,7 @@ struct Walk {
     __device__ __forceinline__ bool next(const GemmParams& p) {
         if (++kb < p.KB) return false;
         kb = 0;
-        if (kDP && r < p.dp_rounds) {
+        if (r < p.dp_rounds) {
             if (++r < p.dp_rounds) {
                 tile += sched_units(p);
             } else {
@@ -248,7 +247,19 @@ struct Walk {
         }
         return true;
     }
-    __device__ __forceinline__ bool in_dp(const GemmParams& p) const { return kDP && r < p.dp_rounds; }
+    __device__ __forceinline__ bool in_dp(const GemmParams& p) const { return r < p.dp_rounds; }
+};
+
+// Ring position (slot, phase parity) advancing by `step` slots per use.
+struct RingPos {
+    uint32_t s, ph;
+    __device__ __forceinline__ void adv(uint32_t step, uint32_t n) {
+        s += step;
+        if (s >= n) {
+            s -= n;
+            ph ^= 1;
+        }
+    }
 };
 
 // linear tile -> (token tile mt, weight tile nt), from the parameter bank
@@ -347,6 +358,7 @@ __device__ __forceinline__ void store_chunk(const GemmParams& p, uint32_t m0, ui
 }
 
 #ifdef LQG_TRACE
+// Debug builds: per-CTA %globaltimer events and per-role wait cycles.
 __device__ unsigned long long g_lqg_trace[8 * 160 * 16];
 __device__ __forceinline__ void trace(uint32_t slot, uint32_t e) {
     uint64_t t;
@@ -355,13 +367,23 @@ __device__ __forceinline__ void trace(uint32_t slot, uint32_t e) {
 }
 #define LQG_T(e) trace(p.trace_slot, e)
 #define LQG_TV(e, v) (g_lqg_trace[(p.trace_slot * 160 + blockIdx.x) * 16 + (e)] = (v))
+#define LQG_WAIT(acc_, call_)                  \
+    do {                                       \
+        const long long t0_ = clock64();       \
+        call_;                                 \
+        acc_ += clock64() - t0_;               \
+    } while (0)
 #else
 #define LQG_T(e) ((void)0)
 #define LQG_TV(e, v) ((void)0)
+#define LQG_WAIT(acc_, call_) call_
 #endif
 
-// kDecode: two CTAs per SM (<= 110 KB SMEM, 256 TMEM columns, <= 72 registers)
-// so consecutive GEMMs overlap under PDL; otherwise one CTA per SM.
+template <uint32_t V>
+struct UConst {
+    static constexpr uint32_t value = V;
+};
+
 // kG > 1: grouped launch over up to kG weight groups (MoE experts).
 // kFan: the epilogue also stores every tile into p.fan[0..n_fan) (fused
 // all-gather of the N-split driver); a separate instantiation so the plain
@@ -370,9 +392,9 @@ __device__ __forceinline__ void trace(uint32_t slot, uint32_t e) {
 // CTA dequantizes its own 128 weight rows into its TMEM and loads half of the
 // activation tile (N/2 tokens); the leader issues one M=256 MMA that reads the
 // B halves from both CTAs' shared memory, which halves the activation
-// shared-memory traffic per SM (the bound at large M).
-template <bool kDecode, uint32_t kG, bool kFan, bool kPair = false>
-__global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
+// shared-memory traffic per SM.
+template <uint32_t kG, bool kFan, bool kPair = false>
+__global__ void __launch_bounds__(kThreads, 1)
     lqg_w4a8_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const GemmParams p,
                          const __grid_constant__ GroupTable<kG> gt) {
     extern __shared__ uint8_t smem_raw[];
@@ -382,44 +404,43 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
     uint8_t* smem = smem_raw + pad;
     const uint32_t smem_base = raw_addr + pad;
 
-    const uint32_t S = p.stages;
-    const uint32_t ring_bytes = S * p.stage_bytes;
-    // barriers after the ring
-    const uint32_t bar_base = smem_base + ring_bytes;
+    const uint32_t SX = p.x_stages, SW = p.w_stages;
+    const uint32_t ring_bytes = p.w_base + SW * p.chunk_bytes;  // X ring, then W ring
+    const uint32_t bar_base = smem_base + ((ring_bytes + 7) & ~7u);
     auto wfull_bar = [&](uint32_t s) { return bar_base + 8 * s; };
-    auto xfull_bar = [&](uint32_t s) { return bar_base + 8 * (kMaxStages + s); };
-    auto empty_bar = [&](uint32_t s) { return bar_base + 8 * (2 * kMaxStages + s); };
-    constexpr uint32_t kB = 3 * kMaxStages;
+    auto wempty_bar = [&](uint32_t s) { return bar_base + 8 * (kMaxStages + s); };
+    auto xfull_bar = [&](uint32_t s) { return bar_base + 8 * (2 * kMaxStages + s); };
+    auto xempty_bar = [&](uint32_t s) { return bar_base + 8 * (3 * kMaxStages + s); };
+    constexpr uint32_t kB = 4 * kMaxStages;
     auto afull_bar = [&](uint32_t a) { return bar_base + 8 * (kB + a); };
     auto aempty_bar = [&](uint32_t a) { return bar_base + 8 * (kB + kMaxASlots + a); };
     auto accfull_bar = [&](uint32_t a) { return bar_base + 8 * (kB + 2 * kMaxASlots + a); };
     auto accempty_bar = [&](uint32_t a) { return bar_base + 8 * (kB + 2 * kMaxASlots + 2 + a); };
     const uint32_t fin_bar = bar_base + 8 * (kB + 2 * kMaxASlots + 4);  // split-K gather (finisher)
-    uint8_t* misc = smem + ring_bytes + 8 * (kB + 2 * kMaxASlots + 5);
+    uint8_t* misc = smem + ((ring_bytes + 7) & ~7u) + 8 * (kB + 2 * kMaxASlots + 5);
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(misc);
     double* ts_s = reinterpret_cast<double*>(misc + 128);  // kMaxBN token scales, as double
 
     const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const uint32_t G = sched_units(p);
-    Sched* sched_s = reinterpret_cast<Sched*>(misc + 32);
     const uint32_t KB = p.KB;
-    const TmemPlan tp = tmem_plan(p.BN, p.tmem_cols);
+    const TmemPlan tp = tmem_plan(p.BN);
     const uint32_t rank = kPair ? ptx::cluster_ctarank() : 0u;  // 0 = pair leader
-    // activation bytes this CTA loads per stage (half of the tile in a pair)
-    const uint32_t x_bytes = (kPair ? p.BN / 2 : p.BN) * kKBlock;
     // barriers the pair leader waits on, as seen from this CTA
     auto leader = [&](uint32_t bar) { return kPair ? ptx::mapa(bar, 0) : bar; };
 
     if (threadIdx.x == 0) LQG_T(0);
     if (threadIdx.x == 0) {
-        *sched_s = make_sched(p);
-        for (uint32_t s = 0; s < S; ++s) {
+        for (uint32_t s = 0; s < SW; ++s) {
             ptx::mbar_init(wfull_bar(s), 1);
+            ptx::mbar_init(wempty_bar(s), 4);  // the 4 warps of the dequant WG of this k-block
+        }
+        for (uint32_t s = 0; s < SX; ++s) {
             ptx::mbar_init(xfull_bar(s), 1);
-            ptx::mbar_init(empty_bar(s), 1);
+            ptx::mbar_init(xempty_bar(s), 1);
         }
         for (uint32_t a = 0; a < kMaxASlots; ++a) {
-            ptx::mbar_init(afull_bar(a), (kPair ? 2 : 1) * Roles<kDecode>::kDQWarps);  // one arrive per dequant warp
+            ptx::mbar_init(afull_bar(a), kPair ? 8 : 4);  // the dequant WG's warps (of both CTAs)
             ptx::mbar_init(aempty_bar(a), 1);
         }
         for (uint32_t a = 0; a < 2; ++a) {
@@ -429,354 +450,291 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
         ptx::mbar_init(fin_bar, 1);
         ptx::fence_mbar_init();
     }
-    if (warp == 0 && lane == 0) ptx::prefetch_tmap(&tmap_x);
-    if (warp == 1) {
+    if (warp == kWarpX && lane == 0) ptx::prefetch_tmap(&tmap_x);
+    if (warp == kWarpMMA) {
         if (kPair)
-            ptx::tmem_alloc_pair(ptx::smem_u32(tmem_holder), p.tmem_cols);
+            ptx::tmem_alloc_pair(ptx::smem_u32(tmem_holder), 512);
         else
-            ptx::tmem_alloc(ptx::smem_u32(tmem_holder), p.tmem_cols);
+            ptx::tmem_alloc(ptx::smem_u32(tmem_holder), 512);
     }
     ptx::tc_fence_before();
     __syncthreads();
     if (kPair) ptx::cluster_sync();  // the peer's barriers are initialised before any remote arrive
     ptx::tc_fence_after();
-    const uint32_t tmem_base = *tmem_holder;
-    const Sched sch = *sched_s;
+    // The CTA owns the SM's whole TMEM (512 columns, one CTA per SM), so the
+    // allocation always starts at lane 0 / column 0: TMEM addresses below are
+    // compile-time offsets (kept in uniform registers by the MMA warp).
+    if (*tmem_holder != 0) __trap();
+    constexpr uint32_t tmem_base = 0;
+    // The schedule is recomputed by every thread from kernel parameters and
+    // the block index (warp-uniform values, no shared-memory round trip).
+    const Sched sch = make_sched(p);
     const uint32_t n_local = sch.n_local;
     // PDL: let the next kernel in the stream start its prologue and weight
-    // prefetch now; everything that reads or writes dependent memory below
+    // stream now; everything that reads or writes dependent memory below
     // (activations, token scales, outputs, workspace) sits behind
     // griddepcontrol.wait.
-    if (threadIdx.x == 0 && p.pdl_trigger == 0) ptx::launch_dependents();
+    if (threadIdx.x == 0) ptx::launch_dependents();
     if (threadIdx.x == 0) LQG_T(1);
 
-    if (warp == 0) {
-        // ------------------------------------------------------------ producer
-        // Weights (static) are streamed immediately: the first min(S, n)
-        // chunks are in flight before griddepcontrol.wait, so the weight
-        // stream of this GEMM overlaps the tail of the previous kernel.
-        // Activation tiles follow the dependency wait.
-        // Reused tiles (activations; weights re-read by several token tiles)
-        // EVICT_LAST, a single-pass weight stream EVICT_FIRST. (Normal
-        // priority via LQG_L2_EVICT_LAST=0 measured ~2 % slower at M = 4096.)
-        const uint64_t pol_w = p.MT == 1 ? ptx::policy_evict_first()
-                                         : (p.l2_last ? ptx::policy_evict_last() : ptx::policy_evict_normal());
-        const uint64_t pol_x = p.l2_last ? ptx::policy_evict_last() : ptx::policy_evict_normal();
-        const uint32_t atom_bytes = (kPair ? p.BN / 2 : p.BN) * kXAtom;
-        // weight walker
-        Walk<!kDecode> ww;
+    if (warp == kWarpW) {
+        // ------------------------------------------------------------ W producer
+        // A single-pass weight stream is EVICT_FIRST; weights re-read by
+        // several token tiles EVICT_LAST.
+        const uint64_t pol_w = p.MT == 1 ? ptx::policy_evict_first() : ptx::policy_evict_last();
+        Walk ww;
         ww.init(sch);
         auto chunk_src = [&](uint32_t tile, uint32_t kb) {
             const TileRef r = tile_ref(tile, p, gt);
             return r.wimg + (uint64_t(r.nt) * KB + kb) * p.chunk_bytes;
         };
         const uint8_t* src = chunk_src(ww.tile, ww.kb);
-        auto w_next = [&]() {
-            if (ww.next(p)) {
-                src = chunk_src(ww.tile, ww.kb);
-            } else {
-                src += p.chunk_bytes;
+        RingPos w{0, 0};
+        for (uint32_t i = 0; i < n_local; ++i) {
+            ptx::mbar_wait(wempty_bar(w.s), w.ph ^ 1);
+            if (ptx::elect_one()) {
+                ptx::mbar_arrive_expect_tx(wfull_bar(w.s), p.chunk_bytes);
+                ptx::bulk_g2s(smem_base + p.w_base + w.s * p.chunk_bytes, src, p.chunk_bytes, wfull_bar(w.s), pol_w);
             }
-        };
-        // weight chunk -> SMEM as w_split concurrent bulk copies (16-byte granular)
-        const uint32_t part = (p.chunk_bytes / p.w_split + 15) / 16 * 16;
-        auto w_copy = [&](uint32_t dst, const uint8_t* gsrc, uint32_t bar) {
-            for (uint32_t off = 0; off < p.chunk_bytes; off += part)
-                ptx::bulk_g2s(dst + off, gsrc + off, min(part, p.chunk_bytes - off), bar, pol_w);
-        };
-        // activation walker
-        Walk<!kDecode> xw;
+            __syncwarp();
+            if (ww.next(p))
+                src = chunk_src(ww.tile, ww.kb);
+            else
+                src += p.chunk_bytes;
+            w.adv(1, SW);
+        }
+    } else if (warp == kWarpX) {
+        // ------------------------------------------------------------ X producer
+        const uint64_t pol_x = ptx::policy_evict_last();
+        const uint32_t atom_bytes = (kPair ? p.BN / 2 : p.BN) * kXAtom;
+        Walk xw;
         xw.init(sch);
         uint32_t xrow0 = tile_ref(xw.tile, p, gt).row0;
-        auto x_issue = [&](uint32_t st) {
-            const uint32_t slot = smem_base + st * p.stage_bytes;
-#ifdef LQG_EXP_NOXTMA
-            ptx::mbar_arrive(xfull_bar(st));  // timing experiment: no activation traffic
-            return;
-#endif
-            const int32_t k0 = int32_t(xw.kb * kKBlock);
-            if (kPair) {
-                // both halves count on the leader's barrier; the leader expects the whole tile
-                if (rank == 0) ptx::mbar_arrive_expect_tx(xfull_bar(st), 2 * x_bytes);
-                const int32_t m0 = int32_t(xrow0 + rank * (p.BN / 2));
-                const uint32_t fb = ptx::mapa(xfull_bar(st), 0);
-                ptx::tma_2d_g2s_pair(slot, &tmap_x, k0, m0, fb, pol_x);
-                ptx::tma_2d_g2s_pair(slot + atom_bytes, &tmap_x, k0 + int32_t(kXAtom), m0, fb, pol_x);
-                return;
-            }
-            ptx::mbar_arrive_expect_tx(xfull_bar(st), x_bytes);
-            const int32_t m0 = int32_t(xrow0);
-            ptx::tma_2d_g2s(slot, &tmap_x, k0, m0, xfull_bar(st), pol_x);
-            ptx::tma_2d_g2s(slot + atom_bytes, &tmap_x, k0 + int32_t(kXAtom), m0, xfull_bar(st),
-                            pol_x);
-        };
-        auto x_next = [&]() {
-            if (xw.next(p)) xrow0 = tile_ref(xw.tile, p, gt).row0;
-        };
-        const uint32_t pre = n_local < S ? n_local : S;
-        for (uint32_t i = 0; i < pre; ++i) {
-            if (ptx::elect_one()) {
-                ptx::mbar_arrive_expect_tx(wfull_bar(i), p.chunk_bytes);
-                w_copy(smem_base + i * p.stage_bytes + x_bytes, src, wfull_bar(i));
-            }
-            __syncwarp();
-            w_next();
-        }
-        // L2 prefetch stream, D = p.l2_prefetch chunks ahead of the SMEM ring:
-        // DRAM latency is covered by L2-resident chunks, so the SMEM ring only
-        // has to cover L2 latency (decode mode keeps it small for co-residency).
-        // The first D chunks are requested before the PDL wait, so HBM keeps
-        // streaming this GEMM's weights while the previous kernel drains.
-        Walk<!kDecode> fw = ww;
-        const uint8_t* fsrc = src;
-        uint32_t pf_issued = pre;  // chunks [pre, pf_issued) requested so far
-        auto pf_next = [&]() {
-            if (fw.next(p)) {
-                fsrc = chunk_src(fw.tile, fw.kb);
-            } else {
-                fsrc += p.chunk_bytes;
-            }
-        };
-        for (; pf_issued < min(n_local, pre + p.l2_prefetch); ++pf_issued) {
-            if (ptx::elect_one()) ptx::prefetch_l2(fsrc, p.chunk_bytes);
-            __syncwarp();
-            pf_next();
-        }
         ptx::griddep_wait();
         if (lane == 0) LQG_T(2);
-        for (uint32_t i = 0; i < pre; ++i) {
-            if (ptx::elect_one()) x_issue(i);
-            __syncwarp();
-            x_next();
-        }
-        uint32_t s = pre == S ? 0 : pre, ph = pre == S ? 1 : 0;
-        for (uint32_t i = pre; i < n_local; ++i) {
-            ptx::mbar_wait(empty_bar(s), ph ^ 1);
-            if (ptx::elect_one()) {
-#ifdef LQG_EXP_NOWTMA
-                ptx::mbar_arrive(wfull_bar(s));
-#else
-                ptx::mbar_arrive_expect_tx(wfull_bar(s), p.chunk_bytes);
-                w_copy(smem_base + s * p.stage_bytes + x_bytes, src, wfull_bar(s));
-#endif
-                x_issue(s);
-                if (pf_issued < n_local) ptx::prefetch_l2(fsrc, p.chunk_bytes);
-            }
-            __syncwarp();
-            if (pf_issued < n_local) {
-                ++pf_issued;
-                pf_next();
-            }
-            w_next();
-            x_next();
-            if (++s == S) {
-                s = 0;
-                ph ^= 1;
-            }
-        }
-        if (lane == 0 && p.pdl_trigger == 1) ptx::launch_dependents();
-    } else if (warp == 1 && (!kPair || rank == 0)) {
-        // ------------------------------------------------------------ MMA issuer
-        const uint32_t idesc = ptx::idesc_i8(kPair ? 2 * kTileN : kTileN, p.BN);
-        const uint64_t desc0 = ptx::sw128_kmajor_desc(smem_base);
-        const uint32_t stage_desc = p.stage_bytes >> 4;
-        const uint32_t atom_desc = ((kPair ? p.BN / 2 : p.BN) * kXAtom) >> 4;
-        Walk<!kDecode> mw;
-        mw.init(sch);
-        bool seg_start = true;
-        uint32_t s = 0, ph = 0, a = 0, aph = 0, as = 0, acc_ph = 0;
-#ifdef LQG_TRACE
-        long long w_acc = 0, w_a = 0, w_x = 0;
-        const long long t_mma0 = clock64();
-#endif
+        RingPos x{0, 0};
         for (uint32_t i = 0; i < n_local; ++i) {
-            const bool seg_end = (mw.kb == KB - 1) || (i + 1 == n_local);
-#ifdef LQG_TRACE
-            const long long tw0 = clock64();
-            if (seg_start) ptx::mbar_wait(accempty_bar(as), acc_ph ^ 1);
-            const long long tw1 = clock64();
-            ptx::mbar_wait(afull_bar(a), aph);
-            const long long tw2 = clock64();
-            ptx::mbar_wait(xfull_bar(s), ph);
-            const long long tw3 = clock64();
-            w_acc += tw1 - tw0;
-            w_a += tw2 - tw1;
-            w_x += tw3 - tw2;
-#else
-            if (seg_start) ptx::mbar_wait(accempty_bar(as), acc_ph ^ 1);
-            ptx::mbar_wait(afull_bar(a), aph);
-            ptx::mbar_wait(xfull_bar(s), ph);
-#endif
-#ifndef LQG_TRACE_DQ
-            if (i == 0 && lane == 0) LQG_T(4);
-            if (i + 1 == n_local && lane == 0) LQG_T(5);
-#endif
-            ptx::tc_fence_after();
+            ptx::mbar_wait(xempty_bar(x.s), x.ph ^ 1);
             if (ptx::elect_one()) {
-                const uint32_t d_tmem = tmem_base + as * tp.acc_stride;
-                const uint32_t a_tmem = tmem_base + tp.a_base + a * kACols;
-                const uint64_t bdesc = desc0 + uint64_t(s * stage_desc);
-#pragma unroll
-                for (uint32_t k8 = 0; k8 < kSubBlocks; ++k8)
-                    if (kPair)
-                        ptx::mma_i8_ts_pair(d_tmem, a_tmem + k8 * 8,
-                                            bdesc + (k8 / 4) * atom_desc + (k8 % 4) * 2, idesc,
-                                            (seg_start && k8 == 0) ? 0u : 1u);
-                    else
-                        ptx::mma_i8_ts(d_tmem, a_tmem + k8 * 8,
-                                       bdesc + (k8 / 4) * atom_desc + (k8 % 4) * 2, idesc,
-                                       (seg_start && k8 == 0) ? 0u : 1u);
+                const uint32_t slot = smem_base + x.s * p.x_slot_bytes;
+                const int32_t k0 = int32_t(xw.kb * kKBlock);
                 if (kPair) {
-                    ptx::mma_commit_pair(empty_bar(s));
-                    ptx::mma_commit_pair(aempty_bar(a));
-                    if (seg_end) ptx::mma_commit_pair(accfull_bar(as));
+                    // both halves count on the leader's barrier; the leader expects the whole tile
+                    if (rank == 0) ptx::mbar_arrive_expect_tx(xfull_bar(x.s), 2 * p.x_slot_bytes);
+                    const int32_t m0 = int32_t(xrow0 + rank * (p.BN / 2));
+                    const uint32_t fb = ptx::mapa(xfull_bar(x.s), 0);
+                    ptx::tma_2d_g2s_pair(slot, &tmap_x, k0, m0, fb, pol_x);
+                    ptx::tma_2d_g2s_pair(slot + atom_bytes, &tmap_x, k0 + int32_t(kXAtom), m0, fb, pol_x);
                 } else {
-                    ptx::mma_commit(empty_bar(s));
-                    ptx::mma_commit(aempty_bar(a));
-                    if (seg_end) ptx::mma_commit(accfull_bar(as));
+                    ptx::mbar_arrive_expect_tx(xfull_bar(x.s), p.x_slot_bytes);
+                    const int32_t m0 = int32_t(xrow0);
+                    ptx::tma_2d_g2s(slot, &tmap_x, k0, m0, xfull_bar(x.s), pol_x);
+                    ptx::tma_2d_g2s(slot + atom_bytes, &tmap_x, k0 + int32_t(kXAtom), m0, xfull_bar(x.s), pol_x);
                 }
             }
             __syncwarp();
+            if (xw.next(p)) xrow0 = tile_ref(xw.tile, p, gt).row0;
+            x.adv(1, SX);
+        }
+    } else if (warp == kWarpMMA && (!kPair || rank == 0)) {
+        // ------------------------------------------------------------ MMA issuer
+        const uint32_t idesc = ptx::idesc_i8(kPair ? 2 * kTileN : kTileN, p.BN);
+        const uint64_t desc0 = ptx::sw128_kmajor_desc(smem_base);
+        const uint32_t slot_desc = p.x_slot_bytes >> 4;
+        const uint32_t atom_desc = ((kPair ? p.BN / 2 : p.BN) * kXAtom) >> 4;
+        // Segment lengths (k-blocks accumulated into one accumulator stage):
+        // dp_rounds whole tiles, then the stream-K range's first (partial)
+        // tile, then whole tiles, the last one possibly cut by the range end.
+        const uint32_t dp_iters = sch.dp_rounds * KB;
+        auto seg_len = [&](uint32_t i) -> uint32_t {
+            if (i < dp_iters) return KB;
+            return min(i == dp_iters ? KB - sch.sk_kb : KB, n_local - i);
+        };
+        uint32_t seg_left = n_local ? seg_len(0) : 0;
+        bool seg_start = true;
+        RingPos x{0, 0}, a{0, 0};
+        uint32_t as = 0, acc_ph = 0;
+#ifdef LQG_TRACE
+        long long w_acc = 0, w_a = 0, w_x = 0, w_issue = 0;
+        const long long t_mma0 = clock64();
+#endif
+        auto wait_ready = [&]() {
+            if (seg_start) LQG_WAIT(w_acc, ptx::mbar_wait(accempty_bar(as), acc_ph ^ 1));
+            LQG_WAIT(w_a, ptx::mbar_wait(afull_bar(a.s), a.ph));
+            LQG_WAIT(w_x, ptx::mbar_wait(xfull_bar(x.s), x.ph));
+            ptx::tc_fence_after();
+        };
+        auto mma = [&](uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t k8, bool first) {
+            const uint64_t bd = bdesc + (k8 / 4) * atom_desc + (k8 % 4) * 2;
+            if (kPair)
+                ptx::mma_i8_ts_pair(d_tmem, a_tmem + k8 * 8, bd, idesc, first ? 0u : 1u);
+            else
+                ptx::mma_i8_ts(d_tmem, a_tmem + k8 * 8, bd, idesc, first ? 0u : 1u);
+        };
+        auto commit = [&](uint32_t bar) {
+            if (kPair)
+                ptx::mma_commit_pair(bar);
+            else
+                ptx::mma_commit(bar);
+        };
+        for (uint32_t i = 0; i < n_local; ++i) {
+            wait_ready();
+            if (i == 0 && lane == 0) LQG_T(4);
+            if (i + 1 == n_local && lane == 0) LQG_T(5);
+            const bool seg_end = seg_left == 1;
+#ifdef LQG_TRACE
+            const long long t_is0 = clock64();
+#endif
+            if (ptx::elect_one()) {
+                const uint32_t d_tmem = tmem_base + as * tp.acc_stride;
+                const uint32_t a_tmem = tmem_base + tp.a_base + a.s * kACols;
+                const uint64_t bdesc = desc0 + uint64_t(x.s * slot_desc);
+#pragma unroll
+                for (uint32_t k8 = 0; k8 < kSubBlocks; ++k8) mma(d_tmem, a_tmem, bdesc, k8, seg_start && k8 == 0);
+                commit(xempty_bar(x.s));
+                commit(aempty_bar(a.s));
+                if (seg_end) commit(accfull_bar(as));
+            }
+            __syncwarp();
+#ifdef LQG_TRACE
+            w_issue += clock64() - t_is0;
+#endif
             if (seg_end && ++as == tp.acc_stages) {
                 as = 0;
                 acc_ph ^= 1;
             }
-            seg_start = mw.next(p);
-            if (++s == S) {
-                s = 0;
-                ph ^= 1;
-            }
-            if (++a == tp.a_slots) {
-                a = 0;
-                aph ^= 1;
-            }
+            seg_start = seg_end;
+            if (--seg_left == 0 && i + 1 < n_local) seg_left = seg_len(i + 1);
+            x.adv(1, SX);
+            a.adv(1, tp.a_slots);
         }
-        if (lane == 0 && p.pdl_trigger == 2) ptx::launch_dependents();
 #ifdef LQG_TRACE
         if (lane == 0) {  // MMA-warp wait cycles: accumulator, A operand, activation tile, total
             LQG_TV(12, (unsigned long long)w_acc);
             LQG_TV(13, (unsigned long long)w_a);
             LQG_TV(14, (unsigned long long)w_x);
             LQG_TV(15, (unsigned long long)(clock64() - t_mma0));
+            LQG_TV(3, (unsigned long long)w_issue);
         }
 #endif
-    } else if (warp >= kDequantWarp0 && warp < Roles<kDecode>::kEpi0) {
+    } else if (warp >= kDequantWarp0 && warp < kEpiWarp0) {
         // ------------------------------------------------------------ dequant WGs
-        // Both warpgroups work on every k-block: WG w dequantizes sub-blocks
-        // [4w, 4w+4). Every waiter therefore observes every phase of every
-        // ring barrier (a parity wait can never alias an older phase).
-        const uint32_t wg = (warp - kDequantWarp0) / 4;  // which part of the k-block
-        const uint32_t sp = warp % 4;            // TMEM sub-partition
-        const uint32_t row = sp * 32 + lane;     // weight row within the tile = TMEM lane
-        const uint32_t lane_addr = (sp * 32) << 16;
-        const uint32_t p_shift = param_shift(p.P);
-        constexpr uint32_t kHalf = kSubBlocks / (Roles<kDecode>::kDQWarps / 4);  // sub-blocks per WG
-        uint32_t s = 0, ph = 0, a = 0, aph = 0;
+        // WG w dequantizes the whole k-blocks w, w+2, w+4, ... of this CTA.
+        // Both rings are even, so WG w always uses the same half of the W
+        // slots and A slots and observes every phase of each (a parity wait
+        // can never alias an older phase).
+        const uint32_t wg = (warp - kDequantWarp0) / 4;
+        const uint32_t sp = warp % 4;         // TMEM sub-partition
+        const uint32_t row = sp * 32 + lane;  // weight row within the tile = TMEM lane
+        const uint32_t a_lane = tmem_base + ((sp * 32) << 16) + tp.a_base;
+        const uint8_t* wring = smem + p.w_base;
+        auto run = [&](auto kp) {
+            constexpr uint32_t P = decltype(kp)::value;
+            constexpr uint32_t kSubPerP = kSubBlocks / P;
 #ifdef LQG_TRACE
-        long long dq_w = 0, dq_a = 0, dq_st = 0, dq_ar = 0;
-        const long long t_dq0 = clock64();
+            long long dq_w = 0, dq_a = 0;
+            const long long t_dq0 = clock64();
 #endif
-        const uint8_t* ring_w = smem + x_bytes;
-        const uint32_t a_base = tmem_base + lane_addr + tp.a_base + wg * kHalf * 8;
-        for (uint32_t i = 0; i < n_local; ++i) {
-#ifdef LQG_TRACE
-            const long long td0 = clock64();
-            ptx::mbar_wait(wfull_bar(s), ph);
-            const long long td1 = clock64();
-            ptx::mbar_wait(aempty_bar(a), aph ^ 1);
-            const long long td2 = clock64();
-            dq_w += td1 - td0;
-            dq_a += td2 - td1;
-#else
-            ptx::mbar_wait(wfull_bar(s), ph);
-            ptx::mbar_wait(aempty_bar(a), aph ^ 1);
-#endif
-            ptx::tc_fence_after();
-            const uint8_t* wchunk = ring_w + s * p.stage_bytes;
-            const uint16_t* prm = reinterpret_cast<const uint16_t*>(wchunk + kCodeBytes);
-            const uint32_t a_taddr = a_base + a * kACols;
-            uint32_t sa[kHalf];
-            uint4 v[kHalf];
+            RingPos w{wg, 0}, a{wg, 0};
+            for (uint32_t i = wg; i < n_local; i += 2) {
+                LQG_WAIT(dq_w, ptx::mbar_wait(wfull_bar(w.s), w.ph));
+                const uint8_t* wchunk = wring + w.s * p.chunk_bytes;
+                // all P group parameters of this row: one 2..16-byte LDS
+                uint32_t prm[(P + 1) / 2];
+                const uint8_t* pa = wchunk + kCodeBytes + row * (2 * P);
+                if constexpr (P == 1) {
+                    prm[0] = *reinterpret_cast<const uint16_t*>(pa);
+                } else if constexpr (P == 2) {
+                    prm[0] = *reinterpret_cast<const uint32_t*>(pa);
+                } else if constexpr (P == 4) {
+                    const uint2 t = *reinterpret_cast<const uint2*>(pa);
+                    prm[0] = t.x;
+                    prm[1] = t.y;
+                } else {
+                    const uint4 t = *reinterpret_cast<const uint4*>(pa);
+                    prm[0] = t.x;
+                    prm[1] = t.y;
+                    prm[2] = t.z;
+                    prm[3] = t.w;
+                }
+                uint4 v[kSubBlocks];
 #pragma unroll
-            for (uint32_t cc = 0; cc < kHalf; ++cc) {
-                const uint32_t c = wg * kHalf + cc;
-#ifdef LQG_EXP_NOLDS
-                sa[cc] = 0x8001u + c;
-                v[cc] = make_uint4(row, c, i, s);
-                (void)prm;
-                (void)wchunk;
-#else
-                sa[cc] = prm[(c >> p_shift) * kTileN + row];
-                v[cc] = *reinterpret_cast<const uint4*>(wchunk + (c * kTileN + row) * 16);
-#endif
-            }
+                for (uint32_t c = 0; c < kSubBlocks; ++c)
+                    v[c] = *reinterpret_cast<const uint4*>(wchunk + (c * kTileN + row) * 16);
+                LQG_WAIT(dq_a, ptx::mbar_wait(aempty_bar(a.s), a.ph ^ 1));
+                ptx::tc_fence_after();
+                const uint32_t a_taddr = a_lane + a.s * kACols;
 #pragma unroll
-            for (uint32_t cc = 0; cc < kHalf; ++cc) {
-                const uint32_t sc = sa[cc] & 0xFFu;
-                const uint32_t a4 = (sa[cc] >> 8) * 0x01010101u;
-                uint32_t o[8];
-#ifdef LQG_EXP_NODEQUANT
-                o[0] = v[cc].x; o[1] = v[cc].y; o[2] = v[cc].z; o[3] = v[cc].w;
-                o[4] = sc; o[5] = a4; o[6] = v[cc].x; o[7] = v[cc].y;
-#else
-                lqq_dequant_word(v[cc].x, sc, a4, o[0], o[1]);
-                lqq_dequant_word(v[cc].y, sc, a4, o[2], o[3]);
-                lqq_dequant_word(v[cc].z, sc, a4, o[4], o[5]);
-                lqq_dequant_word(v[cc].w, sc, a4, o[6], o[7]);
-#endif
-                ptx::tmem_st_x8(a_taddr + cc * 8, o);
+                for (uint32_t h = 0; h < 2; ++h) {
+                    uint32_t o[32];
+#pragma unroll
+                    for (uint32_t cc = 0; cc < 4; ++cc) {
+                        const uint32_t c = 4 * h + cc;
+                        const uint32_t pi = c / kSubPerP;  // parameter region of sub-block c
+                        const uint32_t sa = (prm[pi / 2] >> (16 * (pi % 2))) & 0xFFFFu;
+                        const uint32_t sc = sa & 0xFFu;
+                        const uint32_t a4 = (sa >> 8) * 0x01010101u;
+                        lqq_dequant_word(v[c].x, sc, a4, o[8 * cc + 0], o[8 * cc + 1]);
+                        lqq_dequant_word(v[c].y, sc, a4, o[8 * cc + 2], o[8 * cc + 3]);
+                        lqq_dequant_word(v[c].z, sc, a4, o[8 * cc + 4], o[8 * cc + 5]);
+                        lqq_dequant_word(v[c].w, sc, a4, o[8 * cc + 6], o[8 * cc + 7]);
+                    }
+                    if (h == 1) {
+                        // every code of the chunk has been consumed: free the W slot
+                        __syncwarp();
+                        if (lane == 0) ptx::mbar_arrive(wempty_bar(w.s));
+                    }
+                    ptx::tmem_st_x32(a_taddr + h * 32, o);
+                }
+                ptx::tmem_st_wait();
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if (kPair && rank != 0)
+                        ptx::mbar_arrive_cluster_relaxed(leader(afull_bar(a.s)));
+                    else
+                        ptx::mbar_arrive(afull_bar(a.s));
+                }
+                w.adv(2, SW);
+                a.adv(2, tp.a_slots);
             }
 #ifdef LQG_TRACE
-            const long long td3 = clock64();
-#endif
-            ptx::tmem_st_wait();
-#ifdef LQG_TRACE
-            const long long td4 = clock64();
-#endif
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) {
-                if (kPair && rank != 0)
-                    ptx::mbar_arrive_cluster_relaxed(leader(afull_bar(a)));
-                else
-                    ptx::mbar_arrive(afull_bar(a));
+            if (warp == kDequantWarp0 && lane == 0) {  // dequant waits: weights, A slot, total
+                LQG_TV(11, (unsigned long long)(clock64() - t_dq0));
+                LQG_TV(9, (unsigned long long)dq_w);
+                LQG_TV(10, (unsigned long long)dq_a);
             }
-#ifdef LQG_TRACE
-            __syncwarp();
-            dq_st += td4 - td3;
-            dq_ar += clock64() - td4;
 #endif
-            if (++s == S) {
-                s = 0;
-                ph ^= 1;
-            }
-            if (++a == tp.a_slots) {
-                a = 0;
-                aph ^= 1;
-            }
+        };
+        switch (p.P) {
+            case 1: run(UConst<1>{}); break;
+            case 2: run(UConst<2>{}); break;
+            case 4: run(UConst<4>{}); break;
+            default: run(UConst<8>{}); break;
         }
-#ifdef LQG_TRACE_DQ  // (with LQG_TRACE) replaces the timeline slots 2-5 and 11
-        if (warp == kDequantWarp0 && lane == 0) {  // dequant waits: weights, A slot, total
-            LQG_TV(2, (unsigned long long)dq_w);
-            LQG_TV(3, (unsigned long long)dq_a);
-            LQG_TV(4, (unsigned long long)dq_st);
-            LQG_TV(5, (unsigned long long)dq_ar);
-            LQG_TV(11, (unsigned long long)(clock64() - t_dq0));
-        }
-#endif
-    } else if (warp >= Roles<kDecode>::kEpi0) {
+    } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
         // ------------------------------------------------------------ epilogue
         const uint32_t sp = warp % 4;
         const uint32_t row = sp * 32 + lane;
         const uint32_t lane_addr = (sp * 32) << 16;
-        const uint32_t et = threadIdx.x - Roles<kDecode>::kEpi0 * 32;  // 0..127
+        const uint32_t et = threadIdx.x - kEpiWarp0 * 32;  // 0..127
         const uint32_t nchunks = p.BN / 16;
         const bool scaled = p.out_kind != kOutAcc;
         ptx::griddep_wait();
         uint32_t as = 0, acc_ph = 0, fin_ph = 0;
         uint32_t i = 0;
-        Walk<!kDecode> ew;
+        Walk ew;
         ew.init(sch);
+        auto release_acc = [&](uint32_t cur_as) {
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if (kPair && rank != 0)
+                    ptx::mbar_arrive_cluster_relaxed(leader(accempty_bar(cur_as)));
+                else
+                    ptx::mbar_arrive(accempty_bar(cur_as));
+            }
+        };
         while (i < n_local) {
             const uint32_t tile = ew.tile;
             const uint32_t kb0 = ew.kb;
@@ -836,16 +794,7 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
                     uint32_t v[16];
                     ptx::tmem_ld_x16(acc_taddr + ch * 16, v);
                     ptx::tmem_ld_wait();
-                    if (ch + 1 == nchunks) {
-                        ptx::tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) {
-                            if (kPair && rank != 0)
-                                ptx::mbar_arrive_cluster_relaxed(leader(accempty_bar(cur_as)));
-                            else
-                                ptx::mbar_arrive(accempty_bar(cur_as));
-                        }
-                    }
+                    if (ch + 1 == nchunks) release_acc(cur_as);
                     if (n < p.N) {
                         int32_t a[16];
 #pragma unroll
@@ -858,22 +807,15 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
                 // segment): publish the INT32 partial into this CTA's cells.
                 // Small tiles: no fence and no flag -- |partial| <= 133120 *
                 // 127^2 < 2^31, so INT32_MIN never occurs as a value and marks
-                // "not published". Large tiles: a release flag per CTA.
+                // "not published"; each 16-byte cell is written by one st.cg
+                // and re-read by the finisher until no lane holds the sentinel.
+                // Large tiles: every cell, then a fence and a release flag per CTA.
                 int32_t* slot = p.parts + uint64_t(blockIdx.x) * kSlotCellsK + (small ? 0u : kSmallCells);
                 for (uint32_t ch = 0; ch < nchunks; ++ch) {
                     uint32_t v[16];
                     ptx::tmem_ld_x16(acc_taddr + ch * 16, v);
                     ptx::tmem_ld_wait();
-                    if (ch + 1 == nchunks) {
-                        ptx::tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) {
-                            if (kPair && rank != 0)
-                                ptx::mbar_arrive_cluster_relaxed(leader(accempty_bar(cur_as)));
-                            else
-                                ptx::mbar_arrive(accempty_bar(cur_as));
-                        }
-                    }
+                    if (ch + 1 == nchunks) release_acc(cur_as);
                     // [chunk][quad q][row] int4 cells: a warp's stores are 512
                     // contiguous bytes, and the finisher's bulk copy is one block
                     int4* cell = reinterpret_cast<int4*>(slot) + ch * 4 * kTileN + row;
@@ -888,7 +830,7 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
                     asm volatile("bar.sync 1, 128;" ::: "memory");
                     if (et == 0) ptx::st_release_u32(p.flags + blockIdx.x, 1u);
                 }
-                if (et == 0) LQG_T(9);
+                if (et == 0) LQG_T(7);
             } else {
                 // Head piece of a split tile: this CTA finishes the tile (in
                 // stream-K order it is the CTA's last segment). Integer addition
@@ -951,10 +893,10 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
                     }
                 } else {
                     // Large token tiles: this is the CTA's last segment, so the
-                    // SMEM ring is idle. Wait (acquire) until every contributor
+                    // SMEM rings are idle. Wait (acquire) until every contributor
                     // has raised its flag, then gather the partials (one
                     // contiguous BN*512-byte block each) by TMA bulk copies, as
-                    // many per batch as the ring holds, and sum them from SMEM:
+                    // many per batch as the rings hold, and sum them from SMEM:
                     // two L2 round trips per batch instead of one per 16-token
                     // chunk. Flags are reset for the next launch (which touches
                     // them only after griddepcontrol.wait).
@@ -967,7 +909,6 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
                         p.flags[fc] = 0;
                     }
                     asm volatile("bar.sync 1, 128;" ::: "memory");
-                    (void)0;
                     for (uint32_t c0 = c_first; c0 < c_end; c0 += nb_max) {
                         const uint32_t nb = min(nb_max, c_end - c0);
                         const bool last_batch = c0 + nb >= c_end;
@@ -976,8 +917,8 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
                             ptx::mbar_arrive_expect_tx(fin_bar, nb * part_bytes);
                             for (uint32_t b = 0; b < nb; ++b)
                                 ptx::bulk_g2s(smem_base + b * part_bytes,
-                                              p.parts + uint64_t(kPair ? 2 * (c0 + b) + rank : c0 + b) * kSlotCellsK + kSmallCells, part_bytes,
-                                              fin_bar, ptx::policy_evict_first());
+                                              p.parts + uint64_t(kPair ? 2 * (c0 + b) + rank : c0 + b) * kSlotCellsK + kSmallCells,
+                                              part_bytes, fin_bar, ptx::policy_evict_first());
                         }
                         ptx::mbar_wait(fin_bar, fin_ph);
                         fin_ph ^= 1;
@@ -1003,7 +944,7 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
                                 // running sum back into the accumulator for the next batch
                                 ptx::tmem_st_x16(acc_taddr + ch * 16, sum);
                             } else {
-                                if (ch == 0 && et == 0) LQG_T(10);
+                                if (ch == 0 && et == 0) LQG_T(8);
                                 if (n < p.N) store_chunk<kFan>(p, m0 + ch * 16, mlim, n, sum, cs, ts_s + ch * 16);
                             }
                         }
@@ -1011,30 +952,21 @@ __global__ void __launch_bounds__(Roles<kDecode>::kThreadsT, kDecode ? 2 : 1)
                         asm volatile("bar.sync 1, 128;" ::: "memory");  // ring reads done before the next batch
                     }
                 }
-                ptx::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) {
-                            if (kPair && rank != 0)
-                                ptx::mbar_arrive_cluster_relaxed(leader(accempty_bar(cur_as)));
-                            else
-                                ptx::mbar_arrive(accempty_bar(cur_as));
-                        }
+                release_acc(cur_as);
             }
             asm volatile("bar.sync 1, 128;" ::: "memory");  // ts_s reuse
         }
     }
 
-    if (warp == Roles<kDecode>::kEpi0 && lane == 0) LQG_T(7);
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
-    if (threadIdx.x == 0) LQG_T(8);
     if (kPair) ptx::cluster_sync();  // the leader's MMAs into this CTA's TMEM are complete
-    if (warp == 1) {
+    if (warp == kWarpMMA) {
         if (kPair)
-            ptx::tmem_dealloc_pair(tmem_base, p.tmem_cols);
+            ptx::tmem_dealloc_pair(tmem_base, 512);
         else
-            ptx::tmem_dealloc(tmem_base, p.tmem_cols);
+            ptx::tmem_dealloc(tmem_base, 512);
     }
 }
 

@@ -11,7 +11,7 @@
 //   streaming one tile's k-blocks reads contiguous HBM.
 //
 //   chunk = codes [8 sub-blocks c][128 rows r][16 B]                 16384 B
-//         + params [P][128 rows] u16 (lo byte s_u8, hi byte a)       256*P B
+//         + params [128 rows r][P] u16 (lo byte s_u8, hi byte a)       256*P B
 //
 //   codes(c, r) holds the 32 UINT4 codes of row r, k = kb*256 + 32c + 0..31,
 //   as four little-endian words; word w carries k-offsets 8w..8w+7 with the
@@ -20,6 +20,8 @@
 //   thread per sub-block; a warp reads 512 contiguous bytes (conflict-free).
 //   After LQQ dequant, word w yields TMEM columns 2w (lo) and 2w+1 (hi) of
 //   sub-block c, i.e. the K-major int8 A operand of tcgen05.mma kind::i8.
+//   A row's P parameters are contiguous (2P bytes), so the dequant thread of
+//   that row fetches all of them with one LDS per k-block.
 //
 //   P = params per k-block: 1 if g % 256 == 0, 2 if g % 128 == 0,
 //   4 if g % 64 == 0, else 8 (g % 32 == 0 required). Param p covers
@@ -55,11 +57,6 @@ inline uint32_t params_per_kblock(uint32_t g) {
     return 8;
 }
 
-// log2(sub-blocks per param): sub-block c uses param c >> shift.
-__host__ __device__ inline uint32_t param_shift(uint32_t P) {
-    return P == 1 ? 3u : (P == 2 ? 2u : (P == 4 ? 1u : 0u));
-}
-
 inline ImageGeom make_geom(uint32_t n, uint32_t k, uint32_t g) {
     ImageGeom G;
     G.n = n;
@@ -81,7 +78,8 @@ __host__ __device__ inline uint64_t code_offset(uint32_t chunk_bytes, uint32_t K
 __host__ __device__ inline uint64_t param_offset(uint32_t chunk_bytes, uint32_t KB, uint32_t row,
                                                  uint32_t kb, uint32_t p) {
     const uint32_t nt = row / kTileN, r = row % kTileN;
-    return (uint64_t(nt) * KB + kb) * chunk_bytes + kCodeBytes + (uint64_t(p) * kTileN + r) * 2;
+    const uint32_t P = (chunk_bytes - kCodeBytes) / 256;
+    return (uint64_t(nt) * KB + kb) * chunk_bytes + kCodeBytes + (uint64_t(r) * P + p) * 2;
 }
 
 }  // namespace lqg

@@ -508,6 +508,37 @@ def quantize_activations(x, out_q=None, out_ts=None, check_finite: bool = False,
     return q, ts
 
 
+def tune_set(name: str, value: int) -> None:
+    """Set a launch-schedule knob (lqg_tune_set; results are bit-identical
+    under every setting)."""
+    check(_lib.lib().lqg_tune_set(name.encode(), int(value)))
+
+
+def tune_get(name: str) -> int:
+    v = C.c_int64()
+    check(_lib.lib().lqg_tune_get(name.encode(), C.byref(v)))
+    return v.value
+
+
+class tune:
+    """Context manager: ``with lq.tune(pair=1): ...`` sets knobs and restores
+    their previous values on exit."""
+
+    def __init__(self, **knobs):
+        self.knobs = knobs
+        self.old = {}
+
+    def __enter__(self):
+        for k, v in self.knobs.items():
+            self.old[k] = tune_get(k)
+            tune_set(k, v)
+        return self
+
+    def __exit__(self, *exc):
+        for k, v in self.old.items():
+            tune_set(k, v)
+
+
 def launch_count() -> int:
     """Kernels launched by liblqg.so in this process."""
     return int(_lib.lib().lqg_kernel_launch_count())

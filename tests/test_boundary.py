@@ -121,9 +121,9 @@ def decode_image(img, n, k, g):
     # element 8w+j in lo nibble of byte j, 8w+j+4 in hi nibble
     el = np.concatenate([lo, hi], axis=-1)                               # nt kb c r w 8
     el = el.transpose(0, 3, 1, 2, 4, 5).reshape(NT * TN, KB * KBLK)       # row, k
-    prm = ch[:, :, TN * KBLK // 2:].reshape(NT, KB, P, TN, 2)
-    s = prm[..., 0].transpose(0, 3, 1, 2).reshape(NT * TN, KB * P)
-    a = prm[..., 1].transpose(0, 3, 1, 2).reshape(NT * TN, KB * P)
+    prm = ch[:, :, TN * KBLK // 2:].reshape(NT, KB, TN, P, 2)              # nt kb r p {s, a}
+    s = prm[..., 0].transpose(0, 2, 1, 3).reshape(NT * TN, KB * P)
+    a = prm[..., 1].transpose(0, 2, 1, 3).reshape(NT * TN, KB * P)
     return el[:n, :k], s, a, P
 
 

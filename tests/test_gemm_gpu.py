@@ -403,16 +403,9 @@ def test_column_parallel_p2p_single_rank(torch_cuda, lqg):
     assert torch.equal(y, layer.dw.gemm(q, ts))
 
 
-def _with_env(name, value, fn):
-    old = os.environ.get(name)
-    os.environ[name] = value
-    try:
+def _with_tune(lqg, fn, **knobs):
+    with lqg.lq.tune(**knobs):
         return fn()
-    finally:
-        if old is None:
-            del os.environ[name]
-        else:
-            os.environ[name] = old
 
 
 @pytest.mark.parametrize("m,n,k", [(400, 256, 1024), (1000, 2048, 4096), (4096, 1024, 8192), (300, 384, 640),
@@ -420,7 +413,7 @@ def _with_env(name, value, fn):
 def test_cta_pair_mode_matches(torch_cuda, lqg, m, n, k):
     """CTA-pair kernel (cluster of two, tcgen05 cta_group::2, M = 256, each
     CTA loading half of every activation tile; the default from 320 tokens)
-    is bit-identical to the one-CTA kernel (LQG_PAIR=0), accumulators and BF16."""
+    is bit-identical to the one-CTA kernel (tune pair=0), accumulators and BF16."""
     torch = torch_cuda
     g = torch.Generator(device="cuda").manual_seed(m + n)
     dw = lqg.DeviceWeights.quantize(torch.randn(n, k, generator=g, device="cuda") * 0.02, 128)
@@ -430,8 +423,8 @@ def test_cta_pair_mode_matches(torch_cuda, lqg, m, n, k):
         r = dw.gemm_accum(q), dw.gemm(q, ts)
         torch.cuda.synchronize()
         return r
-    acc0, y0 = _with_env("LQG_PAIR", "0", run)
-    acc1, y1 = _with_env("LQG_PAIR", "1", run)
+    acc0, y0 = _with_tune(lqg, run, pair=0)
+    acc1, y1 = _with_tune(lqg, run, pair=1)
     assert torch.equal(acc0, acc1) and torch.equal(y0, y1)
 
 
@@ -446,8 +439,8 @@ def test_cta_pair_mode_matches_oracle(torch_cuda, lqg, port, m, n, k, g):
     q, ts = port.quantize_activations(make_acts(rng, m, k))
     acc_ref, y_ref = port.gemm_oracle(q, ts, port.bundle_int8(b), b["channel_scales"])
     xq, tsd = torch.from_numpy(q).cuda(), torch.from_numpy(ts).cuda()
-    acc = _with_env("LQG_PAIR", "1", lambda: dw.gemm_accum(xq).cpu().numpy())
-    y = _with_env("LQG_PAIR", "1", lambda: dw.gemm(xq, tsd, out_dtype=torch.float32).cpu().numpy())
+    acc = _with_tune(lqg, lambda: dw.gemm_accum(xq).cpu().numpy(), pair=1)
+    y = _with_tune(lqg, lambda: dw.gemm(xq, tsd, out_dtype=torch.float32).cpu().numpy(), pair=1)
     np.testing.assert_array_equal(acc.astype(np.int64), acc_ref)
     np.testing.assert_array_equal(y.view(np.uint32), y_ref.view(np.uint32))
 
@@ -462,3 +455,32 @@ def test_pair_threshold_boundary_is_seamless(torch_cuda, lqg):
     a319, y319 = dw.gemm_accum(q[:319]), dw.gemm(q[:319], ts[:319])
     a320, y320 = dw.gemm_accum(q), dw.gemm(q, ts)
     assert torch.equal(a319, a320[:319]) and torch.equal(y319, y320[:319])
+
+
+@pytest.mark.parametrize("m,n,k", [(1, 640, 2304), (16, 1024, 4096), (48, 512, 1280), (130, 768, 2048),
+                                   (200, 256, 8192), (700, 512, 1536)])
+@pytest.mark.parametrize("knobs", [dict(max_w_stages=2), dict(max_w_stages=4, x_ring_bytes=1024),
+                                   dict(max_x_stages=2, x_ring_bytes=1024), dict(grid=7), dict(grid=64, no_dp=1),
+                                   dict(max_bn=32), dict(pair=1, pair_single_tile=1), dict(no_pdl=1)])
+def test_schedule_knobs_bit_exact(torch_cuda, lqg, m, n, k, knobs):
+    """Every ring split (2-stage W ring, minimal X ring), grid size, token
+    tile and pair policy gives the same INT32 accumulators and BF16 outputs as
+    the default schedule: the decoupled W/X rings, the alternating dequant
+    warpgroups and the split-K exchange are exercised at their edges."""
+    torch = torch_cuda
+    g = torch.Generator(device="cuda").manual_seed(m * 7 + n + k)
+    dw = lqg.DeviceWeights.quantize(torch.randn(n, k, generator=g, device="cuda") * 0.02, 128)
+    q, ts = lqg.quantize_activations(torch.randn(m, k, generator=g, device="cuda"))
+    acc0, y0 = dw.gemm_accum(q), dw.gemm(q, ts)
+    with lqg.tune(**knobs):
+        acc1, y1 = dw.gemm_accum(q), dw.gemm(q, ts)
+    torch.cuda.synchronize()
+    assert torch.equal(acc0, acc1) and torch.equal(y0, y1)
+
+
+def test_tune_rejects_unknown_and_out_of_range(lqg):
+    with pytest.raises(lqg.ValidationError):
+        lqg.tune_set("no_such_knob", 1)
+    with pytest.raises(lqg.ValidationError):
+        lqg.tune_set("max_w_stages", 1)
+    assert lqg.tune_get("pair") == -1

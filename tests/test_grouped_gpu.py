@@ -98,18 +98,14 @@ def test_grouped_rejects_bad_groups(torch_cuda, lqg):
 @pytest.mark.parametrize("ms,n,k", [([700, 0, 333, 1200, 5], 1024, 2048), ([321, 322], 512, 4096)])
 def test_grouped_pair_mode_equals_one_cta(torch_cuda, lqg, ms, n, k):
     """Grouped launches use CTA pairs from 320 tokens in the largest group;
-    bit-identical to the one-CTA grouped kernel (LQG_PAIR=0)."""
-    import os
+    bit-identical to the one-CTA grouped kernel (tune pair=0)."""
     torch = torch_cuda
     g = torch.Generator(device="cuda").manual_seed(sum(ms) + n)
     dws = [lqg.DeviceWeights.quantize(torch.randn(n, k, generator=g, device="cuda") * 0.02, 128) for _ in ms]
     xq, ts = lqg.quantize_activations(torch.randn(sum(ms), k, generator=g, device="cuda"))
     res = {}
     for mode in ("0", "1"):
-        os.environ["LQG_PAIR"] = mode
-        try:
+        with lqg.lq.tune(pair=int(mode)):
             res[mode] = (lqg.gemm_grouped_accum(dws, xq, ms), lqg.gemm_grouped(dws, xq, ts, ms))
             torch.cuda.synchronize()
-        finally:
-            del os.environ["LQG_PAIR"]
     assert torch.equal(res["0"][0], res["1"][0]) and torch.equal(res["0"][1], res["1"][1])

@@ -1,0 +1,120 @@
+// Read-bandwidth ceiling for the decode mainloop's access pattern: every CTA
+// streams contiguous chunks of a >L2 buffer into a shared-memory ring with
+// 1-D bulk TMA (cp.async.bulk, one elected producer thread, mbarrier
+// full/empty hand-off, consumer warps that only touch one word per chunk),
+// and, for comparison, a plain LDG.128 grid-stride read.
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 \
+//        -I paper_2509_01229_b200/csrc tools/hbm_stream_probe.cu -o /tmp/hbm_probe -lcuda
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <vector>
+
+#include "sm100_ptx.cuh"
+
+using namespace lqg;
+
+__global__ void __launch_bounds__(256, 1) bulk_stream(const uint8_t* buf, uint64_t chunks_total, uint32_t chunk,
+                                                      uint32_t stages, uint32_t* sink) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const uint32_t base = ptx::smem_u32(smem);
+    const uint32_t bar = base + stages * chunk;
+    auto full = [&](uint32_t s) { return bar + 8 * s; };
+    auto empty = [&](uint32_t s) { return bar + 8 * (16 + s); };
+    const uint32_t warp = threadIdx.x / 32;
+    const uint32_t nw = blockDim.x / 32 - 1;  // consumer warps
+    if (threadIdx.x == 0) {
+        for (uint32_t s = 0; s < stages; ++s) {
+            ptx::mbar_init(full(s), 1);
+            ptx::mbar_init(empty(s), nw);
+        }
+        ptx::fence_mbar_init();
+    }
+    __syncthreads();
+    // contiguous range of chunks per CTA
+    const uint64_t c0 = chunks_total * blockIdx.x / gridDim.x, c1 = chunks_total * (blockIdx.x + 1) / gridDim.x;
+    const uint64_t n = c1 - c0;
+    if (warp == 0) {
+        if (ptx::elect_one()) {
+            const uint64_t pol = ptx::policy_evict_first();
+            uint32_t s = 0, ph = 0;
+            for (uint64_t i = 0; i < n; ++i) {
+                ptx::mbar_wait(empty(s), ph ^ 1);
+                ptx::mbar_arrive_expect_tx(full(s), chunk);
+                ptx::bulk_g2s(base + s * chunk, buf + (c0 + i) * chunk, chunk, full(s), pol);
+                if (++s == stages) { s = 0; ph ^= 1; }
+            }
+        }
+    } else {
+        uint32_t s = 0, ph = 0, acc = 0;
+        for (uint64_t i = 0; i < n; ++i) {
+            ptx::mbar_wait(full(s), ph);
+            acc += reinterpret_cast<const uint32_t*>(smem + s * chunk)[threadIdx.x];
+            __syncwarp();
+            if ((threadIdx.x & 31) == 0) ptx::mbar_arrive(empty(s));
+            if (++s == stages) { s = 0; ph ^= 1; }
+        }
+        if (acc == 0x12345678u) sink[0] = acc;
+    }
+}
+
+__global__ void ldg_stream(const uint4* buf, uint64_t n16, uint32_t* sink) {
+    uint32_t acc = 0;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n16; i += uint64_t(gridDim.x) * blockDim.x) {
+        uint4 v = __ldcs(buf + i);
+        acc ^= v.x ^ v.y ^ v.z ^ v.w;
+    }
+    if (acc == 0x12345678u) sink[0] = acc;
+}
+
+int main() {
+    const uint64_t bytes = 2ull << 30;
+    uint8_t* buf;
+    uint32_t* sink;
+    cudaMalloc(&buf, bytes);
+    cudaMalloc(&sink, 4);
+    cudaMemset(buf, 1, bytes);
+    int sms;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    cudaFuncSetAttribute(bulk_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    auto timeit = [&](auto&& f) {
+        f();
+        cudaDeviceSynchronize();
+        float best = 1e9;
+        for (int r = 0; r < 5; ++r) {
+            cudaEventRecord(e0);
+            f();
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            float ms;
+            cudaEventElapsedTime(&ms, e0, e1);
+            best = ms < best ? ms : best;
+        }
+        return best;
+    };
+    for (uint32_t chunk : {8192u, 16896u, 33792u}) {
+        for (uint32_t stages : {4u, 8u, 12u}) {
+            if (stages * chunk + 512 > 227 * 1024) continue;
+            for (int cps : {1}) {
+                const uint64_t nchunks = bytes / chunk;
+                float ms = timeit([&] {
+                    bulk_stream<<<sms * cps, 256, stages * chunk + 512>>>(buf, nchunks, chunk, stages, sink);
+                });
+                printf("bulk chunk=%6u stages=%2u grid=%d: %.1f GB/s\n", chunk, stages, sms * cps,
+                       nchunks * chunk / (ms * 1e-3) / 1e9);
+            }
+        }
+    }
+    for (int blocks : {sms, 2 * sms, 4 * sms, 8 * sms}) {
+        float ms = timeit([&] { ldg_stream<<<blocks, 512>>>(reinterpret_cast<const uint4*>(buf), bytes / 16, sink); });
+        printf("ldg grid=%d x 512: %.1f GB/s\n", blocks, bytes / (ms * 1e-3) / 1e9);
+    }
+    cudaError_t err = cudaGetLastError();
+    printf("status: %s\n", cudaGetErrorString(err));
+    return 0;
+}
