@@ -344,7 +344,11 @@ int alloc_weights(int dev, const ImageGeom& G, lqg_weights** out) {
 // Token tile: <= 192 so that the INT32 accumulator stays double-buffered in
 // TMEM (2 x 192 columns + a 2-slot A ring, see tmem_plan).
 constexpr uint32_t kMaxTileM = 192;
-constexpr uint32_t kPairMinM = 320;  // CTA pairs from this many tokens (largest group)
+// CTA pairs from this many tokens (largest group), also with a single token
+// tile: one M = 256 MMA per k-block serves two SMs, which halves the MMA
+// warp's per-k-block overhead per SM (LLaMA-2-70B 4-GEMM step on B200:
+// M = 128 117 -> 110 us, M = 256 176 -> 159 us; M = 16 unchanged either way).
+constexpr uint32_t kPairMinM = 48;
 constexpr uint32_t kDecodeWStages = 6;  // W ring depth for token tiles <= 32
 constexpr uint32_t kMaxGroups = 64;  // experts per grouped launch
 // Dynamic shared memory: the two rings, then barriers / schedule / token scales.
@@ -367,7 +371,7 @@ constexpr TuneDef kTuneDefs[kTuneCount] = {
     {"max_bn", kMaxTileM, 16, kMaxTileM},          // token-tile cap
     {"pair_min_m", kPairMinM, 1, 1 << 30},         // CTA pairs from this many tokens
     {"pair", -1, -1, 1},                           // -1 auto, 0 never, 1 wherever legal
-    {"pair_single_tile", 0, 0, 1},                 // allow pairs with one token tile
+    {"pair_single_tile", 1, 0, 1},                 // allow pairs with one token tile
     {"x_ring_bytes", 0, 0, kSmemMax},              // 0 = balanced rings; else reserve for X
     {"max_x_stages", kMaxStages, 2, kMaxStages},
     {"max_w_stages", kMaxStages, 2, kMaxStages},
@@ -586,7 +590,9 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
     const uint32_t w_cap = BN <= 32 ? kDecodeWStages : kMaxStages;
     uint32_t sw = std::min({ring_budget / (p.x_slot_bytes + G.chunk_bytes), K.max_w_stages, w_cap}) & ~1u;
     if (K.x_ring_bytes) sw = std::min(sw, std::max(2u, ((ring_budget - std::min(ring_budget, K.x_ring_bytes)) / G.chunk_bytes) & ~1u));
-    p.x_stages = std::min({(ring_budget - sw * G.chunk_bytes) / p.x_slot_bytes, K.max_x_stages, kMaxStages});
+    // even: the dequant warpgroups (which wait on the X tiles, see the
+    // kernel) alternate k-blocks
+    p.x_stages = std::min({(ring_budget - sw * G.chunk_bytes) / p.x_slot_bytes, K.max_x_stages, kMaxStages}) & ~1u;
     if (p.x_stages < 2) return set_err(LQG_EVALIDATION, "tile configuration does not fit shared memory");
     p.w_base = p.x_stages * p.x_slot_bytes;
     // A split-K finisher of a large token tile gathers each contributor's

@@ -16,11 +16,13 @@
 //                 previous kernel).
 //   warp 14       X producer: two 2-D SW128 tensor copies of the activation
 //                 tile per k-block into the X ring (after griddepcontrol.wait).
-//   warp 1        MMA issuer (+ TMEM allocation, 512 columns): 8 x
-//                 tcgen05.mma.kind::i8 (K = 32 each) per k-block, A from
-//                 TMEM, B from the X ring; tcgen05.commit frees the X slot
-//                 and the TMEM A slot and signals the epilogue at the end of
-//                 a tile segment.
+//   warp 1        MMA issuer (+ TMEM allocation, 512 columns): one barrier
+//                 wait per k-block (afull: the dequant warps publish the A
+//                 slot only once the k-block's activation tile has landed
+//                 too), 8 x tcgen05.mma.kind::i8 (K = 32 each), A from TMEM,
+//                 B from the X ring; tcgen05.commit frees the X slot and the
+//                 TMEM A slot and signals the epilogue at the end of a tile
+//                 segment.
 //   warps 2-9     two dequant warpgroups (the paper's ImFP compute WGs,
 //                 P:415-416) taking alternate k-blocks: LDS of the packed
 //                 codes and group parameters (one 2..16-byte LDS per k-block
@@ -490,7 +492,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         const uint8_t* src = chunk_src(ww.tile, ww.kb);
         RingPos w{0, 0};
+#ifdef LQG_EXP_MMAONLY
+        for (uint32_t i = 0; i < 0; ++i) {
+#else
         for (uint32_t i = 0; i < n_local; ++i) {
+#endif
             ptx::mbar_wait(wempty_bar(w.s), w.ph ^ 1);
             if (ptx::elect_one()) {
                 ptx::mbar_arrive_expect_tx(wfull_bar(w.s), p.chunk_bytes);
@@ -515,7 +521,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         RingPos x{0, 0};
         for (uint32_t i = 0; i < n_local; ++i) {
             ptx::mbar_wait(xempty_bar(x.s), x.ph ^ 1);
+#if defined(LQG_EXP_NOX) || defined(LQG_EXP_MMAONLY)  // timing experiments only: no activation loads (garbage B)
+            if (ptx::elect_one() && (!kPair || rank == 0)) ptx::mbar_arrive(xfull_bar(x.s));
+            if (false) {
+#else
             if (ptx::elect_one()) {
+#endif
                 const uint32_t slot = smem_base + x.s * p.x_slot_bytes;
                 const int32_t k0 = int32_t(xw.kb * kKBlock);
                 if (kPair) {
@@ -555,13 +566,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         RingPos x{0, 0}, a{0, 0};
         uint32_t as = 0, acc_ph = 0;
 #ifdef LQG_TRACE
-        long long w_acc = 0, w_a = 0, w_x = 0, w_issue = 0;
+        long long w_acc = 0, w_a = 0, w_x = 0, w_issue = 0;  // w_x: unused (X folded into afull)
         const long long t_mma0 = clock64();
 #endif
         auto wait_ready = [&]() {
             if (seg_start) LQG_WAIT(w_acc, ptx::mbar_wait(accempty_bar(as), acc_ph ^ 1));
+#ifndef LQG_EXP_NOAWAIT  // timing experiment: MMA does not wait for the dequant (garbage A)
             LQG_WAIT(w_a, ptx::mbar_wait(afull_bar(a.s), a.ph));
-            LQG_WAIT(w_x, ptx::mbar_wait(xfull_bar(x.s), x.ph));
+#endif
             ptx::tc_fence_after();
         };
         auto mma = [&](uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t k8, bool first) {
@@ -635,8 +647,29 @@ __global__ void __launch_bounds__(kThreads, 1)
             long long dq_w = 0, dq_a = 0;
             const long long t_dq0 = clock64();
 #endif
-            RingPos w{wg, 0}, a{wg, 0};
+            RingPos w{wg, 0}, a{wg, 0}, xr{wg, 0};
+            // The activation tile of this k-block must have landed before the
+            // A operand is published: the MMA warp then waits on a single
+            // barrier (afull) per k-block. In a pair the leader's barrier
+            // counts both CTAs' halves, so only the leader's warps wait.
+            auto wait_x = [&]() {
+                if (!kPair || rank == 0) ptx::mbar_wait(xfull_bar(xr.s), xr.ph);
+                xr.adv(2, SX);
+            };
             for (uint32_t i = wg; i < n_local; i += 2) {
+#ifdef LQG_EXP_MMAONLY
+                ptx::mbar_wait(aempty_bar(a.s), a.ph ^ 1);
+                wait_x();
+                __syncwarp();
+                if (lane == 0) {
+                    if (kPair && rank != 0)
+                        ptx::mbar_arrive_cluster_relaxed(leader(afull_bar(a.s)));
+                    else
+                        ptx::mbar_arrive(afull_bar(a.s));
+                }
+                a.adv(2, tp.a_slots);
+                continue;
+#endif
                 LQG_WAIT(dq_w, ptx::mbar_wait(wfull_bar(w.s), w.ph));
                 const uint8_t* wchunk = wring + w.s * p.chunk_bytes;
                 // all P group parameters of this row: one 2..16-byte LDS
@@ -658,9 +691,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                     prm[3] = t.w;
                 }
                 uint4 v[kSubBlocks];
+#ifdef LQG_EXP_NODQ  // timing experiment only: no code loads (garbage A)
+#pragma unroll
+                for (uint32_t c = 0; c < kSubBlocks; ++c) v[c] = make_uint4(row, c, i, prm[0]);
+#else
 #pragma unroll
                 for (uint32_t c = 0; c < kSubBlocks; ++c)
                     v[c] = *reinterpret_cast<const uint4*>(wchunk + (c * kTileN + row) * 16);
+#endif
                 LQG_WAIT(dq_a, ptx::mbar_wait(aempty_bar(a.s), a.ph ^ 1));
                 ptx::tc_fence_after();
                 const uint32_t a_taddr = a_lane + a.s * kACols;
@@ -684,10 +722,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                         __syncwarp();
                         if (lane == 0) ptx::mbar_arrive(wempty_bar(w.s));
                     }
+#ifdef LQG_EXP_NOSTTM  // timing experiment only: A never written (garbage A)
+                    if (o[0] == 0x12345678u && o[31] == 0x9abcdef0u) ptx::tmem_st_x32(a_taddr + h * 32, o);
+#else
                     ptx::tmem_st_x32(a_taddr + h * 32, o);
+#endif
                 }
                 ptx::tmem_st_wait();
                 ptx::tc_fence_before();
+                wait_x();
                 __syncwarp();
                 if (lane == 0) {
                     if (kPair && rank != 0)
@@ -779,7 +822,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (small) load_batch(c_first, 0);
             }
             asm volatile("bar.sync 1, 128;" ::: "memory");
+#ifdef LQG_EXP_SPINACC
+            ptx::mbar_wait(accfull_bar(as), acc_ph);
+#else
             ptx::mbar_wait_parked(accfull_bar(as), acc_ph);  // idle for a tile mainloop
+#endif
             if (i >= n_local && et == 0) LQG_T(6);
             ptx::tc_fence_after();
             const uint32_t acc_taddr = tmem_base + lane_addr + as * tp.acc_stride;

@@ -412,7 +412,7 @@ def _with_tune(lqg, fn, **knobs):
                                    (8192, 512, 1024), (333, 8192, 1024)])
 def test_cta_pair_mode_matches(torch_cuda, lqg, m, n, k):
     """CTA-pair kernel (cluster of two, tcgen05 cta_group::2, M = 256, each
-    CTA loading half of every activation tile; the default from 320 tokens)
+    CTA loading half of every activation tile; the default from 48 tokens)
     is bit-identical to the one-CTA kernel (tune pair=0), accumulators and BF16."""
     torch = torch_cuda
     g = torch.Generator(device="cuda").manual_seed(m + n)
@@ -446,15 +446,15 @@ def test_cta_pair_mode_matches_oracle(torch_cuda, lqg, port, m, n, k, g):
 
 
 def test_pair_threshold_boundary_is_seamless(torch_cuda, lqg):
-    """m = 319 (one-CTA kernel) and m = 320 (pair kernel by default) agree on
+    """m = 47 (one-CTA kernel) and m = 48 (pair kernel by default) agree on
     their common rows: the automatic switch never changes results."""
     torch = torch_cuda
     g = torch.Generator(device="cuda").manual_seed(319)
     dw = lqg.DeviceWeights.quantize(torch.randn(1024, 2048, generator=g, device="cuda") * 0.02, 128)
-    q, ts = lqg.quantize_activations(torch.randn(320, 2048, generator=g, device="cuda"))
-    a319, y319 = dw.gemm_accum(q[:319]), dw.gemm(q[:319], ts[:319])
+    q, ts = lqg.quantize_activations(torch.randn(48, 2048, generator=g, device="cuda"))
+    a319, y319 = dw.gemm_accum(q[:47]), dw.gemm(q[:47], ts[:47])
     a320, y320 = dw.gemm_accum(q), dw.gemm(q, ts)
-    assert torch.equal(a319, a320[:319]) and torch.equal(y319, y320[:319])
+    assert torch.equal(a319, a320[:47]) and torch.equal(y319, y320[:47])
 
 
 @pytest.mark.parametrize("m,n,k", [(1, 640, 2304), (16, 1024, 4096), (48, 512, 1280), (130, 768, 2048),
