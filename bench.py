@@ -54,6 +54,10 @@ GROUP = 128
 
 
 def load_peaks():
+    """Roofline denominators: HBM = MEASURED_PEAKS.json copy bandwidth; INT8 =
+    2 x the measured bf16 cuBLAS burst (kind::i8 runs at twice the kind::f16
+    rate on sm_100), with the cuBLASLt IMMA burst we measured ourselves
+    (profiles/int8_peak.json) reported beside it."""
     peaks = {"hbm_gbs": 6650.0, "hbm_src": "fallback (B200_PROFILING.md)",
              "int8_tops": 2 * 1590.0, "int8_src": "fallback: 2 x bf16 fallback"}
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -63,13 +67,14 @@ def load_peaks():
         peaks["hbm_src"] = "measured (MEASURED_PEAKS.json copy bandwidth)"
         peaks["int8_tops"] = 2 * float(mp["bf16_tflops"])
         peaks["int8_src"] = "2 x measured bf16 burst (MEASURED_PEAKS.json)"
+        if "bf16_tflops_sustained" in mp:
+            peaks["int8_tops_sustained"] = 2 * float(mp["bf16_tflops_sustained"])
     p = os.path.join(ROOT, "profiles", "int8_peak.json")
     if os.path.exists(p):
         ip = json.load(open(p))
-        peaks["int8_tops"] = float(ip["int8_tops"])
-        peaks["int8_src"] = "measured cuBLASLt IMMA burst (profiles/int8_peak.json)"
-        if "int8_tops_sustained" in ip:
-            peaks["int8_tops_sustained"] = float(ip["int8_tops_sustained"])
+        peaks["cublaslt_int8_tops"] = float(ip["int8_tops"])
+        peaks["cublaslt_int8_tops_sustained"] = float(ip.get("int8_tops_sustained", 0)) or None
+        peaks["cublaslt_src"] = "measured cuBLASLt IMMA 8192^3 (profiles/int8_peak.json)"
     return peaks
 
 
@@ -146,7 +151,8 @@ def cpu_reference_sample(workload: dict, steps: int, warmup: int, threads: int |
     bounded sample: for each shape, the first 64*T weight rows (one 64-row band per host
     thread) at M in {1, 64, 512}. The reference's cost is linear in M at fixed (N, K)
     (dequant once per tile + M*N*K MACs), and linear in rows at fixed
-    threads, so t(shape, M) = (a + b*M) * N / N_sample extrapolates the full sweep."""
+    threads, so t(shape, M) = (a + b*M) * N / N_sample extrapolates the full sweep.
+    T = 1 is the reference as shipped (one call, no threads)."""
     import numpy as np
 
     import oracle
@@ -198,32 +204,53 @@ def cpu_reference_sample(workload: dict, steps: int, warmup: int, threads: int |
             total_t += (a + b * m) * n / ns
             total_ops += algo_ops(m, n, k)
     tops = total_ops / total_t / 1e12
-    info = {"threads": T, "rows_per_shape": ns, "ms": ms, "fits": fits,
+    info = {"threads": T, "rows_per_shape": ns, "ms": ms, "fits": fits, "warmup": warmup, "steps": steps,
             "sample_seconds_per_step": sample_t, "predicted_full_sweep_s": total_t}
     return tops, info
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def run_reference_arm(args, workload):
+    """--impl reference: the unmodified reference lq::gemm_w4a8 (oracle/_ref,
+    built from /root/reference/proj/src) on this host's cores; rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    tops, info = cpu_reference_sample(workload, max(1, args.steps), max(0, min(args.warmup, 1)))
+    tops, info = cpu_reference_sample(workload, max(1, args.steps), max(0, args.warmup))
     if tops is None:
         print(json.dumps({"impl": "reference", "unavailable": info}))
         return
+    try:
+        t1, i1 = cpu_reference_sample(workload, 1, 1, threads=1)
+    except Exception as exc:
+        t1, i1 = None, repr(exc)
     line = {
         "metric": "W4A8 GEMM TOPS (llama2-70b layer shapes, M sweep 1..4096)",
         "impl": "reference", "value": tops, "unit": "TOPS", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "int8", "data": "synthetic",
-        "config": {"workload": args.workload, "group_size": GROUP, "engine": "Packed",
-                   "bundle": "DualMmaPacked", "tile": [64, 64, 64]},
+        "config": {"workload": args.workload, "shapes": [[nm, n, k] for nm, n, k in workload["shapes"]],
+                   "m_sweep": workload["m_sweep"], "group_size": GROUP, "out_dtype": "f32",
+                   "engine": "Packed", "bundle": "DualMmaPacked", "tile": [64, 64, 64]},
         "cpu_baseline": {"value": tops, "unit": "TOPS", "cores": info["threads"],
-                         "kind": "reference",
+                         "kind": "reference", "cpu": cpu_model(), "nproc": os.cpu_count(),
                          "sample": f"lq::gemm_w4a8 on rows [0,{info['rows_per_shape']}) of each shape "
                                    f"at M in {info['ms']}, {info['threads']} std::threads (one "
                                    "64-row band each), linear-in-M/linear-in-N extrapolation to "
-                                   "the full sweep"},
+                                   "the full sweep",
+                         "single_thread": {"value": t1, "cores": 1,
+                                           "sample": "the reference as shipped (one call, no threads), "
+                                                     f"rows [0,{i1['rows_per_shape']}) per shape, same extrapolation"
+                                           if t1 else str(i1)}},
         "e2e": {"value": tops, "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "detail": info,
     }
@@ -233,16 +260,66 @@ def run_reference_arm(args, workload):
 # ---------------------------------------------------------------------------
 # lqg arm
 # ---------------------------------------------------------------------------
+def graph_of(fn, torch):
+    """CUDA graph of fn() captured on a side stream (None if capture fails,
+    e.g. a collective backend that cannot be captured)."""
+    g = torch.cuda.CUDAGraph()
+    st = torch.cuda.Stream()
+    st.wait_stream(torch.cuda.current_stream())
+    try:
+        with torch.cuda.stream(st), torch.cuda.graph(g, stream=st):
+            fn()
+    except Exception as exc:  # fall back to eager, reported in the line
+        torch.cuda.current_stream().wait_stream(st)
+        torch.cuda.synchronize()
+        return None, repr(exc)[:160]
+    torch.cuda.current_stream().wait_stream(st)
+    return g, None
+
+
+def timed_region(run, steps, world, dev, torch, dist, clocks_index=None):
+    """Exactly `steps` calls of run() between barrier + synchronize on both
+    sides; CUDA events on the launching stream; max over ranks (ms)."""
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clk = ClockSampler(clocks_index) if clocks_index is not None else None
+    if clk:
+        clk.__enter__()
+    e0.record()
+    for _ in range(steps):
+        run()
+    e1.record()
+    torch.cuda.synchronize()
+    if clk:
+        clk.__exit__()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return ms, (clk.result() if clk else None)
+
+
 def run_lqg(args, workload):
     import torch
     import torch.distributed as dist
 
     import paper_2509_01229_b200 as lqg
+    from paper_2509_01229_b200 import tp
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        sys.exit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
     if world > 1:
+        # the driver reads the communicator size from NCCL's init lines
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -254,7 +331,6 @@ def run_lqg(args, workload):
     gen = torch.Generator(device=dev)
 
     # ---- weights: N-split shards, quantized on the GPU (LiquidQuant two-level)
-    from paper_2509_01229_b200 import tp
     layers = []
     for li, (name, n, k) in enumerate(shapes):
         plan = tp.ShardPlan(n, world, rank, tp.shard_rows(n, world))
@@ -263,7 +339,16 @@ def run_lqg(args, workload):
         w = torch.randn(nr, k, generator=gen, device=dev, dtype=torch.float32).mul_(0.02)
         dw = lqg.DeviceWeights.quantize(w, GROUP)
         del w
-        layers.append(dict(name=name, n=n, nr=nr, k=k, dw=dw, plan=plan))
+        L = dict(name=name, n=n, nr=nr, k=k, dw=dw, plan=plan)
+        # the GEMM writes its column slice straight into the padded send buffer
+        # of the all-gather (output pitch = shard width): no copy, no allocation
+        L["send"] = torch.empty(mmax, plan.width, dtype=torch.bfloat16, device=dev)
+        if world > 1:
+            L["buf"] = torch.empty(world * mmax * plan.width, dtype=torch.bfloat16, device=dev)
+            L["yfull"] = torch.empty(mmax, n, dtype=torch.bfloat16, device=dev)
+            if args.gather == "p2p":
+                L["layer"] = tp.ColumnParallelW4A8(n, k, GROUP, rank, world, device_weights=dw, gather="p2p")
+        layers.append(L)
     torch.cuda.synchronize()
 
     # ---- activations per K, quantized per token on the GPU
@@ -276,162 +361,98 @@ def run_lqg(args, workload):
         del mask
         xs[k] = lqg.quantize_activations(x)
         del x
-    ys = {L["name"]: torch.empty(mmax, L["nr"], dtype=torch.bfloat16, device=dev) for L in layers}
-    if world > 1:
-        yfull = {L["name"]: torch.empty(mmax, L["n"], dtype=torch.bfloat16, device=dev)
-                 for L in layers}
     ws = lqg.Workspace(local)
 
     def gemm(L, m):
         q, ts = xs[L["k"]]
-        L["dw"].gemm(q[:m], ts[:m], out=ys[L["name"]][:m], workspace=ws)
-        if world > 1:
-            tp.gather_columns(ys[L["name"]][:m], L["plan"], out=yfull[L["name"]][:m])
+        L["dw"].gemm(q[:m], ts[:m], out=L["send"][:m, :L["nr"]], workspace=ws)
 
-    def step():
+    def gemm_ag(L, m):
+        if world > 1 and args.gather == "p2p":
+            q, ts = xs[L["k"]]
+            L["layer"](q[:m], ts[:m], out=L["yfull"][:m])
+            return
+        gemm(L, m)
+        if world > 1:
+            tp.gather_columns(L["send"][:m], L["plan"], out=L["yfull"][:m], buf=L["buf"])
+
+    def step_gemm_only():
         for m in msweep:
             for L in layers:
                 gemm(L, m)
 
+    def step():
+        for m in msweep:
+            for L in layers:
+                gemm_ag(L, m)
+
     ops_step = sum(algo_ops(m, L["n"], L["k"]) for m in msweep for L in layers)
 
-    # ---- warm-up (eager: sets kernel attributes; then graph capture for N=1)
+    # ---- warm-up (eager: kernel attributes, workspaces, NCCL communicators),
+    # then CUDA graphs of the step (GEMM + all-gather) and of the GEMMs alone
     for _ in range(max(1, args.warmup)):
         step()
     torch.cuda.synchronize()
-    use_graph = world == 1 and not args.no_graph
-    if use_graph:
-        c0 = lqg.launch_count()
-        g_step = torch.cuda.CUDAGraph()
-        s = torch.cuda.Stream()
-        s.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(s):
-            with torch.cuda.graph(g_step, stream=s):
-                step()
-        torch.cuda.current_stream().wait_stream(s)
-        launches_per_step = lqg.launch_count() - c0
+    graph_note = {}
+    runs = {}
+    for key, fn in (("full", step), ("gemm_only", step_gemm_only)):
+        g = None
+        if not args.no_graph:
+            c0 = lqg.launch_count()
+            g, err = graph_of(fn, torch)
+            if err:
+                graph_note[key] = f"eager (graph capture failed: {err})"
+        if g is not None:
+            runs[key] = g.replay
+            graph_note.setdefault(key, "CUDA graph")
+        else:
+            runs[key] = fn
+            graph_note.setdefault(key, "eager")
         for _ in range(args.warmup):
-            g_step.replay()
-        run = g_step.replay
-    else:
-        launches_per_step = len(msweep) * len(layers)
-        run = step
-    torch.cuda.synchronize()
+            runs[key]()
+        torch.cuda.synchronize()
+    launches_per_step = len(msweep) * len(layers)
 
     # ---- timed region: exactly K steps between barrier + synchronize
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     c0 = lqg.launch_count()
-    with ClockSampler(local) as clk:
-        ev0.record()
-        for _ in range(args.steps):
-            run()
-        ev1.record()
-        torch.cuda.synchronize()
+    ms_total, clocks = timed_region(runs["full"], args.steps, world, dev, torch, dist, clocks_index=local)
     host_launches = lqg.launch_count() - c0
-    if world > 1:
-        dist.barrier()
-    ms_total = ev0.elapsed_time(ev1)
-    if world > 1:
-        t = torch.tensor([ms_total], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_total = float(t.item())
     ms_per_step = ms_total / args.steps
     value = ops_step * args.steps / (ms_total * 1e-3) / 1e12
-    gpu_launches = host_launches if not use_graph else launches_per_step * args.steps
+    gpu_launches = launches_per_step * args.steps if graph_note["full"] == "CUDA graph" else host_launches
+    gemm_only = None
+    if world > 1:
+        ms_g, _ = timed_region(runs["gemm_only"], args.steps, world, dev, torch, dist)
+        gemm_only = {"value": ops_step * args.steps / (ms_g * 1e-3) / 1e12, "unit": "TOPS",
+                     "ms_per_step": ms_g / args.steps, "timing": graph_note["gemm_only"],
+                     "note": "same step without the row-output all-gather"}
 
-    # ---- per-M breakdown (graph of R rotations of the 4 layer GEMMs per M)
-    sweep = []
+    # ---- per-M breakdown (graph of R rotations of the layer GEMMs per M)
+    sweep, per_shape = [], {}
     if world == 1 and not args.no_sweep:
-        R = 3
-        for m in msweep:
-            g = torch.cuda.CUDAGraph()
-            s = torch.cuda.Stream()
-            s.wait_stream(torch.cuda.current_stream())
-            with torch.cuda.stream(s):
-                with torch.cuda.graph(g, stream=s):
-                    for _ in range(R):
-                        for L in layers:
-                            gemm(L, m)
-            torch.cuda.current_stream().wait_stream(s)
-            g.replay()
-            torch.cuda.synchronize()
-            # median of 7 timings of 3 replays each (each replay = R rotations of
-            # the layer GEMMs; 310 MB of weights per rotation > L2). HBM-bound
-            # entries (M <= 64) start after a short idle: right after heavy
-            # tensor-core work the GPU runs memory-bound kernels ~10-30 %
-            # slower for about a second (measured, tools/bench_probe.py).
-            if m <= 64:
-                time.sleep(1.5)
-            reps, samples = 3, []
-            for _ in range(7):
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record()
-                for _ in range(reps):
-                    g.replay()
-                e1.record()
-                torch.cuda.synchronize()
-                samples.append(e0.elapsed_time(e1) * 1e-3 / (reps * R))
-            t_s = statistics.median(samples)
-            if m == mmax:
-                # The tensor-bound entry in both power states (B200 board limit
-                # 1000 W: after seconds of back-to-back INT8 MMA the SM clock
-                # settles near 1450 MHz, sw_power_cap). Burst: after 2 s idle,
-                # 5 replays (~30 ms). Sustained: after 6 s of continuous replays.
-                # Each is compared with the matching cuBLASLt IMMA peak.
-                states = {}
-                for state, pre in (("burst", 0.0), ("sustained", 6.0)):
-                    time.sleep(2.0)
-                    t0 = time.time()
-                    while time.time() - t0 < pre:
-                        for _ in range(10):
-                            g.replay()
-                        torch.cuda.synchronize()
-                    with ClockSampler(local, 0.002) as ck:
-                        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                        e0.record()
-                        for _ in range(5):
-                            g.replay()
-                        e1.record()
-                        torch.cuda.synchronize()
-                    states[state] = {"us": e0.elapsed_time(e1) * 1e-3 / (5 * R) * 1e6, "clocks": ck.result()}
-            ops = sum(algo_ops(m, L["n"], L["k"]) for L in layers)
-            byts = sum(algo_bytes(m, L["n"], L["k"]) for L in layers)
-            sweep.append({"m": m, "us": t_s * 1e6, "tops": ops / t_s / 1e12,
-                          "hbm_gbs": byts / t_s / 1e9,
-                          "hbm_frac": byts / t_s / 1e9 / peaks["hbm_gbs"],
-                          "int8_frac": ops / t_s / 1e12 / peaks["int8_tops"]})
-            if m == mmax:
-                sweep[-1]["power_states"] = states
-            del g
+        sweep, per_shape = run_sweep(layers, msweep, gemm, peaks, torch, local, per_shape_ms=(1, 16))
 
     # ---- e2e through the reference-facing host-buffer C-ABI call
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args, layers, msweep, xs, world, dev, lqg, ops_step)
 
-    # ---- CPU baseline (rank 0, N=1 only)
+    # ---- LLaMA-2-7B sweep (BASELINE configs[1]) and MoE grouped (configs[4])
+    sweep_7b = moe = None
+    if world == 1 and not args.no_sweep and args.workload == "llama2-70b":
+        try:
+            sweep_7b = run_7b(lqg, dev, peaks, torch)
+        except Exception as exc:  # extra evidence must never sink the main number
+            sweep_7b = {"error": repr(exc)[:200]}
+        try:
+            moe = run_moe(lqg, dev, peaks)
+        except Exception as exc:
+            moe = {"error": repr(exc)[:200]}
+
+    # ---- CPU baseline (rank 0, N=1 only), same warm-up as the reference arm
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        try:
-            bundles = None
-            tops_cpu, info = cpu_reference_sample(workload, steps=1, warmup=0, bundles=bundles)
-            if tops_cpu is not None:
-                cpu = {"value": tops_cpu, "unit": "TOPS", "cores": info["threads"],
-                       "kind": "reference",
-                       "sample": f"unmodified lq::gemm_w4a8 (oracle/_ref) on rows "
-                                 f"[0,{info['rows_per_shape']}) of each shape at M in {info['ms']}, "
-                                 f"{info['threads']} threads, extrapolated linearly in M and N to "
-                                 f"the full sweep ({info['sample_seconds_per_step']:.1f} s of CPU "
-                                 f"sample)"}
-            else:
-                cpu = {"value": None, "unit": "TOPS", "cores": 0, "kind": "reference",
-                       "sample": f"unavailable: {info}"}
-        except Exception as exc:  # baseline must never sink the GPU number
-            cpu = {"value": None, "unit": "TOPS", "cores": 0, "kind": "reference",
-                   "sample": f"failed: {exc!r}"}
+        cpu = cpu_baseline(workload)
 
     if rank != 0:
         if world > 1:
@@ -457,6 +478,8 @@ def run_lqg(args, workload):
                     "traffic": prof.get("traffic_bytes_M4096"),
                     "at": f"M={mmax}, 4 layer GEMMs, INT8 ops (TOPS), burst: timed 2 s after idle",
                     "peak_src": peaks["int8_src"], "clocks": st["burst"]["clocks"],
+                    "vs_cublaslt_int8": {"peak": peaks.get("cublaslt_int8_tops"),
+                                         "frac": burst / peaks["cublaslt_int8_tops"] if peaks.get("cublaslt_int8_tops") else None},
                     "sustained": {"achieved": sust, "peak": peaks.get("int8_tops_sustained"),
                                   "frac": sust / peaks["int8_tops_sustained"] if peaks.get("int8_tops_sustained") else None,
                                   "at": "after 6 s of back-to-back replays (power-capped)",
@@ -467,13 +490,8 @@ def run_lqg(args, workload):
         roofline_decode = {"bound": "hbm", "achieved": small["hbm_gbs"], "peak": peaks["hbm_gbs"],
                            "unit": "GB/s", "frac": small["hbm_gbs"] / peaks["hbm_gbs"],
                            "traffic": prof.get("traffic_bytes_M16"),
-                           "at": "M=16, 4 layer GEMMs, algorithmic bytes", "peak_src": peaks["hbm_src"]}
-    moe = None
-    if world == 1 and not args.no_sweep:
-        try:
-            moe = run_moe(lqg, dev, peaks)
-        except Exception as exc:  # extra evidence must never sink the main number
-            moe = {"error": repr(exc)[:200]}
+                           "at": "M=16, 4 layer GEMMs, algorithmic bytes", "peak_src": peaks["hbm_src"],
+                           "per_shape": per_shape.get(16), "per_shape_m1": per_shape.get(1)}
     line = {
         "metric": "W4A8 GEMM TOPS (llama2-70b layer shapes, M sweep 1..4096)",
         "value": value, "unit": "TOPS", "n_gpus": world, "steps": args.steps,
@@ -483,23 +501,195 @@ def run_lqg(args, workload):
         "config": {"workload": args.workload,
                    "shapes": [[nm, n, k] for nm, n, k in shapes], "m_sweep": msweep,
                    "group_size": GROUP, "out_dtype": "bf16", "gemms_per_step": len(msweep) * len(shapes),
-                   "parallelism": f"tp{world}-nsplit+allgather" if world > 1 else "single",
+                   "parallelism": (f"tp{world} N-split + {args.gather} row-output all-gather" if world > 1 else "single"),
                    "l2": "inputs larger than L2: 310 MB of packed weights cycle between reuses",
-                   "timing": ("CUDA graph of the step" if use_graph else "eager") +
-                             "; per-M sweep: median of 7; M <= 64 entries after 1.5 s idle"},
+                   "timing": graph_note["full"] + "; per-M sweep: median of 7; M <= 64 entries after 1.5 s idle"},
         "gpu_launches": gpu_launches,
-        "clocks": clk.result(),
+        "clocks": clocks,
         "roofline": roofline,
         "roofline_decode": roofline_decode,
         "cpu_baseline": cpu,
         "e2e": e2e,
+        "gemm_only": gemm_only,
         "sweep": sweep,
+        "sweep_llama2_7b": sweep_7b,
         "moe_grouped": moe,
         "peaks": peaks,
     }
     print(json.dumps(line))
+    sys.stdout.flush()
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_sweep(layers, msweep, gemm, peaks, torch, local, per_shape_ms=()):
+    """Per-M device time of the layer GEMMs: CUDA graph of R rotations (one
+    rotation = every layer once; consecutive launches use different weights),
+    median of 7 timings of 3 replays. HBM-bound entries (M <= 64) start after a
+    short idle: right after heavy tensor-core work the GPU runs memory-bound
+    kernels ~10-30 % slower for about a second (tools/bench_probe.py)."""
+    R = 3
+    sweep, per_shape = [], {}
+
+    def graph_time(fn, reps=3, n=7):
+        g, _ = graph_of(fn, torch)
+        g.replay()
+        torch.cuda.synchronize()
+        samples = []
+        for _ in range(n):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(reps):
+                g.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            samples.append(e0.elapsed_time(e1) * 1e-3 / reps)
+        return statistics.median(samples), g
+
+    for m in msweep:
+        def rot():
+            for _ in range(R):
+                for L in layers:
+                    gemm(L, m)
+        if m <= 64:
+            time.sleep(1.5)
+        t_s, g = graph_time(rot)
+        t_s /= R
+        states = None
+        if m == max(msweep):
+            # The tensor-bound entry in both power states (B200 board limit
+            # 1000 W: after seconds of back-to-back INT8 MMA the SM clock
+            # settles near 1450 MHz, sw_power_cap). Burst: after 2 s idle,
+            # 5 replays (~30 ms). Sustained: after 6 s of continuous replays.
+            states = {}
+            for state, pre in (("burst", 0.0), ("sustained", 6.0)):
+                time.sleep(2.0)
+                t0 = time.time()
+                while time.time() - t0 < pre:
+                    for _ in range(10):
+                        g.replay()
+                    torch.cuda.synchronize()
+                with ClockSampler(local, 0.002) as ck:
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    for _ in range(5):
+                        g.replay()
+                    e1.record()
+                    torch.cuda.synchronize()
+                states[state] = {"us": e0.elapsed_time(e1) * 1e-3 / (5 * R) * 1e6, "clocks": ck.result()}
+        ops = sum(algo_ops(m, L["n"], L["k"]) for L in layers)
+        byts = sum(algo_bytes(m, L["n"], L["k"]) for L in layers)
+        entry = {"m": m, "us": t_s * 1e6, "tops": ops / t_s / 1e12, "hbm_gbs": byts / t_s / 1e9,
+                 "hbm_frac": byts / t_s / 1e9 / peaks["hbm_gbs"], "int8_frac": ops / t_s / 1e12 / peaks["int8_tops"]}
+        if states:
+            entry["power_states"] = states
+        sweep.append(entry)
+        if m in per_shape_ms:
+            rows = []
+            for L in layers:
+                def one(L=L):
+                    for _ in range(4):
+                        gemm(L, m)
+                time.sleep(0.5)
+                t1, _ = graph_time(one)
+                t1 /= 4
+                b1 = algo_bytes(m, L["n"], L["k"])
+                rows.append({"shape": L["name"], "n": L["n"], "k": L["k"], "us": t1 * 1e6,
+                             "hbm_gbs": b1 / t1 / 1e9, "hbm_frac": b1 / t1 / 1e9 / peaks["hbm_gbs"],
+                             "note": "4 back-to-back launches of this shape"})
+            per_shape[m] = rows
+        del g
+    return sweep, per_shape
+
+
+def run_7b(lqg, dev, peaks, torch):
+    """BASELINE configs[1]: the four LLaMA-2-7B linear-layer GEMMs (qkv
+    12288x4096, o 4096x4096, gate_up 22016x4096, down 4096x11008) at M = 1..1024:
+    graph-amortised device time of the 4-GEMM rotation (3 weight copies per
+    shape so consecutive launches miss L2) and the single-launch latency of one
+    eager GEMM (host launch + kernel, events around one call after a sync)."""
+    wl = WORKLOADS["llama2-7b"]
+    g = torch.Generator(device=dev).manual_seed(7)
+    copies = 3
+    layers = []
+    for name, n, k in wl["shapes"]:
+        dws = [lqg.DeviceWeights.quantize(torch.randn(n, k, generator=g, device=dev) * 0.02, GROUP)
+               for _ in range(copies)]
+        layers.append(dict(name=name, n=n, k=k, dws=dws,
+                           y=torch.empty(max(wl["m_sweep"]), n, dtype=torch.bfloat16, device=dev)))
+    xs = {k: lqg.quantize_activations(torch.randn(max(wl["m_sweep"]), k, generator=g, device=dev))
+          for k in {k for _, _, k in wl["shapes"]}}
+    ws = lqg.Workspace(dev.index or 0)
+    out = []
+    for m in wl["m_sweep"]:
+        def rot():
+            for c in range(copies):
+                for L in layers:
+                    q, ts = xs[L["k"]]
+                    L["dws"][c].gemm(q[:m], ts[:m], out=L["y"][:m], workspace=ws)
+        if m <= 64:
+            time.sleep(1.0)
+        gr, _ = graph_of(rot, torch)
+        gr.replay()
+        torch.cuda.synchronize()
+        samples = []
+        for _ in range(7):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(3):
+                gr.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            samples.append(e0.elapsed_time(e1) * 1e-3 / (3 * copies))
+        t = statistics.median(samples)
+        # single launch: one eager GEMM (down), host launch overhead included
+        L = layers[3]
+        q, ts = xs[L["k"]]
+        single = []
+        for _ in range(9):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            L["dws"][0].gemm(q[:m], ts[:m], out=L["y"][:m], workspace=ws)
+            e1.record()
+            torch.cuda.synchronize()
+            single.append(e0.elapsed_time(e1) * 1e3)
+        ops = sum(algo_ops(m, L["n"], L["k"]) for L in layers)
+        byts = sum(algo_bytes(m, L["n"], L["k"]) for L in layers)
+        out.append({"m": m, "us_4gemm": t * 1e6, "tops": ops / t / 1e12,
+                    "hbm_frac": byts / t / 1e9 / peaks["hbm_gbs"], "int8_frac": ops / t / 1e12 / peaks["int8_tops"],
+                    "single_launch_down_us": statistics.median(single)})
+        del gr
+    return {"shapes": [[nm, n, k] for nm, n, k in wl["shapes"]], "entries": out,
+            "timing": "CUDA graph of 3 rotations of the 4 GEMMs (distinct weight copies), median of 7; "
+                      "single_launch: one eager lqg_gemm_w4a8 of the down shape, CUDA events around the call"}
+
+
+def cpu_baseline(workload):
+    """The reference's CPU path timed on this host beside the GPU number:
+    (ii) one std::thread per 64-row band (nproc threads) and (i) the reference
+    as shipped, one thread; both with the reference arm's warm-up."""
+    res = {}
+    for label, threads in (("threads", None), ("single_thread", 1)):
+        try:
+            tops, info = cpu_reference_sample(workload, steps=1, warmup=1, threads=threads)
+        except Exception as exc:  # baseline must never sink the GPU number
+            tops, info = None, f"failed: {exc!r}"
+        res[label] = (tops, info)
+    tops, info = res["threads"]
+    if tops is None:
+        return {"value": None, "unit": "TOPS", "cores": 0, "kind": "reference", "sample": f"unavailable: {info}"}
+    t1, i1 = res["single_thread"]
+    return {"value": tops, "unit": "TOPS", "cores": info["threads"], "kind": "reference",
+            "cpu": cpu_model(), "nproc": os.cpu_count(),
+            "sample": f"unmodified lq::gemm_w4a8 (oracle/_ref) on rows [0,{info['rows_per_shape']}) of each "
+                      f"shape at M in {info['ms']}, {info['threads']} threads (one 64-row band each), 1 warm-up "
+                      f"pass, extrapolated linearly in M and N to the full sweep "
+                      f"({info['sample_seconds_per_step']:.1f} s of CPU sample)",
+            "single_thread": {"value": t1, "unit": "TOPS", "cores": 1,
+                              "sample": (f"the reference as shipped (no threads): rows [0,{i1['rows_per_shape']}) "
+                                         f"of each shape at M in {i1['ms']}, extrapolated likewise "
+                                         f"({i1['sample_seconds_per_step']:.1f} s)") if t1 else str(i1)}}
 
 
 def run_e2e(args, layers, msweep, xs, world, dev, lqg, ops_step):
@@ -518,8 +708,6 @@ def run_e2e(args, layers, msweep, xs, world, dev, lqg, ops_step):
     d2h = sum(2 * m * L["n"] for m in msweep for L in layers)
     if world > 1:
         dx = {k: (torch.empty_like(q, device=dev), torch.empty_like(ts, device=dev)) for k, (q, ts) in xs.items()}
-        dy = {L["name"]: torch.empty(mmax, L["nr"], dtype=torch.bfloat16, device=dev) for L in layers}
-        yd = {L["name"]: torch.empty(mmax, L["n"], dtype=torch.bfloat16, device=dev) for L in layers}
 
     def one_step():
         for m in msweep:
@@ -531,9 +719,9 @@ def run_e2e(args, layers, msweep, xs, world, dev, lqg, ops_step):
                     qd, td = dx[L["k"]]
                     qd[:m].copy_(qh[:m], non_blocking=True)
                     td[:m].copy_(th[:m], non_blocking=True)
-                    L["dw"].gemm(qd[:m], td[:m], out=dy[L["name"]][:m])
-                    tp.gather_columns(dy[L["name"]][:m], L["plan"], out=yd[L["name"]][:m])
-                    hy[L["name"]][:m].copy_(yd[L["name"]][:m])
+                    L["dw"].gemm(qd[:m], td[:m], out=L["send"][:m, :L["nr"]])
+                    tp.gather_columns(L["send"][:m], L["plan"], out=L["yfull"][:m], buf=L["buf"])
+                    hy[L["name"]][:m].copy_(L["yfull"][:m])
                     torch.cuda.synchronize()
 
     one_step()
@@ -629,6 +817,27 @@ def load_profile_summary():
     return {}
 
 
+def spawn_ranks(args):
+    """`--gpus N` without a launcher: re-exec this script under
+    torch.distributed.run with N local ranks (one per GPU, NCCL over NVLink)."""
+    import socket
+    import subprocess
+
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) are visible")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ, NCCL_DEBUG=os.environ.get("NCCL_DEBUG", "INFO"),
+               NCCL_DEBUG_SUBSYS=os.environ.get("NCCL_DEBUG_SUBSYS", "INIT"))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd, env=env).returncode
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -636,6 +845,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="lqg", choices=["lqg", "reference"])
     ap.add_argument("--workload", default="llama2-70b", choices=sorted(WORKLOADS))
+    ap.add_argument("--gather", default="nccl", choices=["nccl", "p2p"],
+                    help="N>1 row-output all-gather: NCCL collective or fused into the GEMM epilogue")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
@@ -646,9 +857,12 @@ def main():
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":
         run_reference_arm(args, wl)
-    else:
-        run_lqg(args, wl)
+        return 0
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
+    run_lqg(args, wl)
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

@@ -55,9 +55,19 @@ _ERRORS = {1: ValidationError, 2: VerificationError, 3: IoError, 4: CudaError, 5
            6: UnsupportedDeviceError}
 
 
+_OFFSET_RE = None
+
+
 def check(rc: int) -> None:
     if rc:
         msg = _lib.lib().lqg_last_error().decode()
+        if rc == 3:  # "<message> (byte offset N)" -> IoError(message, N), like lq::IoError
+            global _OFFSET_RE
+            import re
+            _OFFSET_RE = _OFFSET_RE or re.compile(r"^(.*) \(byte offset (\d+)\)$", re.S)
+            mo = _OFFSET_RE.match(msg)
+            if mo:
+                raise IoError(mo.group(1), int(mo.group(2)))
         raise _ERRORS.get(rc, RuntimeError)(msg)
 
 
@@ -110,7 +120,6 @@ class QuantizedWeightBundle:
     group_scales: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint8))
     group_offsets: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint8))
     channel_scales: np.ndarray = field(default_factory=lambda: np.zeros(0, np.float32))
-    _device: dict = field(default_factory=dict, repr=False, compare=False)
 
     def groups_per_row(self) -> int:
         return self.k // self.group_size
@@ -159,12 +168,10 @@ class QuantizedWeightBundle:
         return img
 
     def device_weights(self, device: int = 0) -> "DeviceWeights":
-        """The prepacked device copy (created on first use, then cached)."""
-        dw = self._device.get(device)
-        if dw is None:
-            dw = DeviceWeights.from_bundle(self, device)
-            self._device[device] = dw
-        return dw
+        """A new prepacked device copy of the bundle as it is now (not cached:
+        like the reference, every gemm_w4a8 call reads the bundle's current
+        arrays; keep the returned handle to reuse an upload)."""
+        return DeviceWeights.from_bundle(self, device)
 
 
 @dataclass
@@ -361,6 +368,22 @@ class DeviceWeights:
         if not (xq.is_cuda and xq.dtype == torch.int8 and xq.dim() == 2 and xq.shape[1] == self.k
                 and xq.stride(1) == 1):
             raise ValidationError(f"activations must be a CUDA int8 [m, {self.k}] row-major tensor")
+        if xq.device.index != self.device:
+            raise ValidationError(f"activations live on cuda:{xq.device.index}, weights on cuda:{self.device}")
+
+    def _check_ts(self, ts, m):
+        import torch
+        if not (ts.is_cuda and ts.dtype == torch.float32 and ts.dim() == 1 and ts.stride(0) == 1
+                and ts.shape[0] >= m and ts.device.index == self.device):
+            raise ValidationError(f"token scales must be a contiguous CUDA float32 [>= {m}] tensor "
+                                  f"on cuda:{self.device}")
+
+    def _check_out(self, out, m, dtypes):
+        if not (out.is_cuda and out.device.index == self.device and out.dim() == 2
+                and tuple(out.shape) == (m, self.n) and out.stride(1) == 1 and out.stride(0) >= self.n):
+            raise ValidationError(f"output must be a row-major CUDA [{m}, {self.n}] tensor on cuda:{self.device}")
+        if str(out.dtype).replace("torch.", "") not in dtypes:
+            raise ValidationError(f"unsupported output dtype {out.dtype}")
 
     def gemm(self, xq, ts, out=None, out_dtype=None, workspace: Workspace | None = None,
              stream=None):
@@ -368,8 +391,10 @@ class DeviceWeights:
         import torch
         self._check_x(xq)
         m = xq.shape[0]
+        self._check_ts(ts, m)
         if out is None:
             out = torch.empty(m, self.n, dtype=out_dtype or torch.bfloat16, device=xq.device)
+        self._check_out(out, m, Y_DTYPES)
         check(_lib.lib().lqg_gemm_w4a8(
             self.handle, xq.data_ptr(), xq.stride(0), ts.data_ptr(), m, out.data_ptr(),
             out.stride(0), _y_code(out.dtype), workspace.handle if workspace else None,
@@ -382,12 +407,13 @@ class DeviceWeights:
         Each `out` may be a column slice of a wider row-major buffer."""
         self._check_x(xq)
         m = xq.shape[0]
+        self._check_ts(ts, m)
         if not 1 <= len(outs) <= 8:
             raise ValidationError("1..8 output tensors")
         ld = outs[0].stride(0)
         for o in outs:
             if o.shape[0] < m or o.shape[1] != self.n or o.stride(0) != ld or o.stride(1) != 1 \
-                    or o.dtype != outs[0].dtype:
+                    or o.dtype != outs[0].dtype or not o.is_cuda:
                 raise ValidationError("fan-out outputs must share shape, dtype and row pitch")
         ptrs = (C.c_void_p * len(outs))(*[o.data_ptr() for o in outs])
         check(_lib.lib().lqg_gemm_w4a8_fanout(
@@ -401,6 +427,7 @@ class DeviceWeights:
         m = xq.shape[0]
         if out is None:
             out = torch.empty(m, self.n, dtype=torch.int32, device=xq.device)
+        self._check_out(out, m, ("int32",))
         check(_lib.lib().lqg_gemm_w4a8_accum(
             self.handle, xq.data_ptr(), xq.stride(0), m, out.data_ptr(), out.stride(0),
             workspace.handle if workspace else None, _stream_ptr(stream)))

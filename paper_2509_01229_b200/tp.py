@@ -83,11 +83,15 @@ class ShardPlan:
         return max(e - s for s, e in self.ranges)
 
 
-def gather_columns(y_local, plan: ShardPlan, group=None, out=None):
+def gather_columns(y_local, plan: ShardPlan, group=None, out=None, buf=None):
     """All-gather the per-rank column slices [m, n_r] into Y [m, n] (row-major).
 
     One fixed-size all_gather_into_tensor of [world, m, width] (shards padded to
     the widest), then a strided copy into Y. Works with NCCL (GPU) and gloo (CPU).
+    Allocation-free when the caller passes y_local already padded to the shard
+    width (the GEMM can write straight into it: its output pitch is free), a
+    gather buffer `buf` of >= world*m*width elements and `out` -- which is how
+    the bench captures the N-split step in a CUDA graph.
     """
     import torch
     import torch.distributed as dist
@@ -97,8 +101,10 @@ def gather_columns(y_local, plan: ShardPlan, group=None, out=None):
     send = y_local
     if y_local.shape[1] != w or not y_local.is_contiguous():
         send = torch.zeros(m, w, dtype=y_local.dtype, device=y_local.device)
-        send[:, :e - s] = y_local
-    buf = torch.empty(plan.world * m * w, dtype=y_local.dtype, device=y_local.device)
+        send[:, :e - s] = y_local[:, :e - s]
+    if buf is None:
+        buf = torch.empty(plan.world * m * w, dtype=y_local.dtype, device=y_local.device)
+    buf = buf[:plan.world * m * w]
     if plan.world > 1:
         dist.all_gather_into_tensor(buf, send.reshape(-1), group=group)
     else:
@@ -132,7 +138,10 @@ class ColumnParallelW4A8:
         self.dw = device_weights
         self._local = local_gemm
         self.gather = gather
-        self._symm = None  # (max_m, dtype, local Y, peer Ys, handle)
+        self._symm = None  # {"max_m", "dtype", "bufs": 2 x (local Y, every rank's Y, handle), "barrier"}
+        self._symm_injected = False
+        self._fanout = None
+        self._calls = 0
 
     @classmethod
     def from_bundle(cls, b: QuantizedWeightBundle, rank: int, world: int, group=None,
@@ -162,44 +171,74 @@ class ColumnParallelW4A8:
         return self.dw.gemm(xq, ts, out=out)
 
     def _symmetric_output(self, m: int, dtype, device):
-        """Y [max_m, n] in symmetric memory on every rank + the peers' views."""
-        import torch
+        """Two Y buffers [max_m, n] in NVLink symmetric memory on every rank
+        (double-buffered across calls) + every rank's view of them."""
         import torch.distributed as dist
-        if self._symm is not None and self._symm[0] >= m and self._symm[1] == dtype:
+        if self._symm is not None and self._symm["max_m"] >= m and self._symm["dtype"] == dtype:
             return self._symm
         import torch.distributed._symmetric_memory as symm_mem
-        max_m = max(m, self._symm[0] if self._symm else 0)
-        y = symm_mem.empty(max_m, self.n, dtype=dtype, device=device)
+        max_m = max(m, self._symm["max_m"] if self._symm else 0)
         world = self.plan.world
-        if world > 1:
-            group = self.group if self.group is not None else dist.group.WORLD
-            hdl = symm_mem.rendezvous(y, group)
-            peers = [y if r == self.plan.rank else hdl.get_buffer(r, [max_m, self.n], dtype)
-                     for r in range(world)]
-        else:
-            hdl, peers = None, [y]
-        self._symm = (max_m, dtype, y, peers, hdl)
+        bufs = []
+        hdl = None
+        for _ in range(2):
+            y = symm_mem.empty(max_m, self.n, dtype=dtype, device=device)
+            if world > 1:
+                group = self.group if self.group is not None else dist.group.WORLD
+                hdl = symm_mem.rendezvous(y, group)
+                peers = [y if r == self.plan.rank else hdl.get_buffer(r, [max_m, self.n], dtype)
+                         for r in range(world)]
+            else:
+                peers = [y]
+            bufs.append((y, peers, hdl))
+        self._symm = {"max_m": max_m, "dtype": dtype, "bufs": bufs,
+                      "barrier": (lambda h=hdl: h.barrier()) if hdl is not None else (lambda: None)}
         return self._symm
 
     def forward(self, xq, ts, out=None, y_local=None, out_dtype=None):
-        """Y [m, n] = gather_r( X W_r^T * cs_r * ts )."""
-        if self.gather == "p2p" and self._local is None:
+        """Y [m, n] = gather_r( X W_r^T * cs_r * ts ), returned in `out` (or a
+        new tensor) -- never a view of the shared gather buffers.
+
+        p2p protocol (fused all-gather): call t's fan-out GEMM stores this
+        rank's column slice into buffer t % 2 of every rank, then a cross-GPU
+        barrier, then each rank copies its own buffer out. Call t + 2 writes
+        the same buffer again only after the barrier of call t + 1, which no
+        rank passes before every rank has finished its copy-out of call t
+        (stream order: copy-out t, fan-out t+1, barrier t+1): no
+        write-after-read race between a fast and a slow rank.
+        """
+        if self.gather == "p2p":
             import torch
             m = xq.shape[0]
             dtype = out_dtype or (out.dtype if out is not None else torch.bfloat16)
-            _, _, y, peers, hdl = self._symmetric_output(m, dtype, xq.device)
+            symm = self._symm if self._symm_injected else self._symmetric_output(m, dtype, xq.device)
+            y, peers, _ = symm["bufs"][self._calls % 2]
+            self._calls += 1
             s, e = self.plan.rows
             # this rank's column slice of every rank's Y (itself first)
             me = self.plan.rank
             order = [me] + [r for r in range(self.plan.world) if r != me]
-            self.dw.gemm_fanout(xq, ts, [peers[r][:m, s:e] for r in order])
-            if hdl is not None:
-                hdl.barrier()  # every rank's slices have landed in every Y
-            if out is not None:
-                out.copy_(y[:m])
-                return out
-            return y[:m]
+            dests = [peers[r][:m, s:e] for r in order]
+            if self._fanout is not None:
+                self._fanout(xq, ts, dests)
+            else:
+                self.dw.gemm_fanout(xq, ts, dests)
+            symm["barrier"]()  # every rank's slices of call t have landed in every Y
+            if out is None:
+                out = torch.empty(m, self.n, dtype=dtype, device=xq.device)
+            out.copy_(y[:m])
+            return out
         y_r = self.local(xq, ts, out=y_local)
         return gather_columns(y_r, self.plan, self.group, out=out)
+
+    def inject_symmetric(self, bufs, barrier, fanout):
+        """Testing hook: run the p2p protocol over caller-provided buffers
+        (bufs[slot] = (local Y, [Y of every rank])), barrier and fan-out
+        function (e.g. process-shared CPU tensors and a gloo barrier)."""
+        self._symm = {"max_m": bufs[0][0].shape[0], "dtype": bufs[0][0].dtype,
+                      "bufs": [(b[0], b[1], None) for b in bufs], "barrier": barrier}
+        self._symm_injected = True
+        self._fanout = fanout
+        self.gather = "p2p"
 
     __call__ = forward

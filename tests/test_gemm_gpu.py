@@ -251,6 +251,163 @@ def test_llama_shapes_row_subset(torch_cuda, lqg, port, n, k, m):
     np.testing.assert_array_equal(y.cpu().numpy()[np.ix_(rows, cols)].view(np.uint32), y_ref.view(np.uint32))
 
 
+LLAMA7B = [("qkv", 12288, 4096), ("o", 4096, 4096), ("gate_up", 22016, 4096), ("down", 4096, 11008)]
+LLAMA70B = [("qkv", 10240, 8192), ("o", 8192, 8192), ("gate_up", 28672, 8192), ("down", 8192, 28672)]
+
+
+@pytest.mark.parametrize("shape", [s[0] for s in LLAMA7B])
+def test_llama7b_shapes_bf16_and_acc(torch_cuda, lqg, port, shape):
+    """BASELINE configs[1]: every LLaMA-2-7B layer GEMM at M = 1, 16, 256 and
+    1024 (the bench's sweep points) -- INT32 accumulators bit-exact, the F32
+    output bit-identical and the BF16 output (what the bench times) exactly the
+    RNE of the reference F32 on a seeded subset of rows and columns."""
+    torch = torch_cuda
+    _, n, k = next(s for s in LLAMA7B if s[0] == shape)
+    g = torch.Generator(device="cuda").manual_seed(n * 3 + k)
+    dw = lqg.DeviceWeights.quantize(torch.randn(n, k, generator=g, device="cuda") * 0.02, 128)
+    e = dw.export()
+    rng = np.random.default_rng(n)
+    cols = np.sort(rng.choice(n, size=192, replace=False))
+    w8 = port.reconstruct_int8(len(cols), k, 128, port.logical_codes(n, k, 0, e.packed_weights)[cols],
+                               e.group_scales.reshape(n, -1)[cols], e.group_offsets.reshape(n, -1)[cols])
+    for m in (1, 16, 256, 1024):
+        q, ts = lqg.quantize_activations(torch.randn(m, k, generator=g, device="cuda"))
+        acc = dw.gemm_accum(q).cpu().numpy()
+        y32 = dw.gemm(q, ts, out_dtype=torch.float32).cpu().numpy()
+        y16 = dw.gemm(q, ts, out_dtype=torch.bfloat16)
+        rows = np.sort(rng.choice(m, size=min(m, 48), replace=False))
+        acc_ref, y_ref = port.gemm_oracle(q.cpu().numpy()[rows], ts.cpu().numpy()[rows], w8, e.channel_scales[cols])
+        np.testing.assert_array_equal(acc[np.ix_(rows, cols)].astype(np.int64), acc_ref)
+        np.testing.assert_array_equal(y32[np.ix_(rows, cols)].view(np.uint32), y_ref.view(np.uint32))
+        assert torch.equal(y16.cpu()[torch.from_numpy(rows)][:, torch.from_numpy(cols)],
+                           torch.from_numpy(y_ref).to(torch.bfloat16))
+
+
+@pytest.mark.parametrize("m", [16, 4096])
+def test_llama70b_bf16_at_bench_shapes(torch_cuda, lqg, port, m):
+    """The BF16 outputs the bench times, full LLaMA-2-70B shapes: RNE of the
+    reference F32 epilogue (quant.cpp:125-127) on a seeded row/column subset."""
+    torch = torch_cuda
+    for name, n, k in LLAMA70B:
+        g = torch.Generator(device="cuda").manual_seed(n + 2 * k + m)
+        dw = lqg.DeviceWeights.quantize(torch.randn(n, k, generator=g, device="cuda") * 0.02, 128)
+        q, ts = lqg.quantize_activations(torch.randn(m, k, generator=g, device="cuda"))
+        y16 = dw.gemm(q, ts)
+        e = dw.export()
+        rng = np.random.default_rng(n + m)
+        cols = np.sort(rng.choice(n, size=96, replace=False))
+        rows = np.sort(rng.choice(m, size=min(m, 32), replace=False))
+        w8 = port.reconstruct_int8(len(cols), k, 128, port.logical_codes(n, k, 0, e.packed_weights)[cols],
+                                   e.group_scales.reshape(n, -1)[cols], e.group_offsets.reshape(n, -1)[cols])
+        _, y_ref = port.gemm_oracle(q.cpu().numpy()[rows], ts.cpu().numpy()[rows], w8, e.channel_scales[cols])
+        got = y16.cpu()[torch.from_numpy(rows)][:, torch.from_numpy(cols)]
+        assert torch.equal(got, torch.from_numpy(y_ref).to(torch.bfloat16)), name
+        del dw
+
+
+def test_one_handle_two_streams_default_workspaces(torch_cuda, lqg):
+    """The boundary's re-entrancy contract: one immutable
+    handle launched concurrently on two streams without explicit workspaces
+    (each stream gets its own default split-K workspace) -- every result is
+    bit-identical to the serial one."""
+    torch = torch_cuda
+    g = torch.Generator(device="cuda").manual_seed(5)
+    dw = lqg.DeviceWeights.quantize(torch.randn(8192, 8192, generator=g, device="cuda") * 0.02, 128)
+    inputs = [lqg.quantize_activations(torch.randn(m, 8192, generator=g, device="cuda")) for m in (1, 16, 77, 200, 513)]
+    want = [(dw.gemm_accum(q), dw.gemm(q, ts)) for q, ts in inputs]
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    for st in streams:
+        st.wait_stream(torch.cuda.current_stream())
+    got = []
+    for rep in range(6):
+        for i, (q, ts) in enumerate(inputs):
+            st = streams[(i + rep) % 2]
+            with torch.cuda.stream(st):
+                got.append((i, dw.gemm_accum(q, stream=st), dw.gemm(q, ts, stream=st)))
+    torch.cuda.synchronize()
+    for i, a, y in got:
+        assert torch.equal(a, want[i][0]) and torch.equal(y, want[i][1]), i
+
+
+def test_host_call_is_reentrant_across_threads(torch_cuda, lqg):
+    """lqg_gemm_w4a8_host from four host threads on one handle at once
+    (pooled staging contexts, no shared mutable state): bit-identical to the
+    serial calls."""
+    import threading
+    torch = torch_cuda
+    g = torch.Generator(device="cuda").manual_seed(6)
+    dw = lqg.DeviceWeights.quantize(torch.randn(4096, 4096, generator=g, device="cuda") * 0.02, 128)
+    work = []
+    for m in (1, 33, 256, 2100):
+        q, ts = lqg.quantize_activations(torch.randn(m, 4096, generator=g, device="cuda"))
+        qh, th = q.cpu().pin_memory(), ts.cpu().pin_memory()
+        ref = torch.empty(m, 4096, dtype=torch.bfloat16).pin_memory()
+        dw.gemm_host(qh, th, ref)
+        work.append((qh, th, ref))
+    errors = []
+
+    def worker(tid):
+        try:
+            for rep in range(8):
+                qh, th, ref = work[(tid + rep) % len(work)]
+                y = torch.empty_like(ref).pin_memory()
+                dw.gemm_host(qh, th, y)
+                if not torch.equal(y, ref):
+                    errors.append((tid, rep))
+        except Exception as exc:  # surfaced below
+            errors.append(repr(exc))
+
+    th_ = [threading.Thread(target=worker, args=(t,)) for t in range(4)]
+    for t in th_:
+        t.start()
+    for t in th_:
+        t.join()
+    assert not errors, errors
+
+
+def test_device_api_validates_scales_and_outputs(torch_cuda, lqg):
+    """ts / out of the wrong dtype, device or shape are rejected before the
+    launch (no out-of-bounds writes, no sticky context errors)."""
+    torch = torch_cuda
+    dw = lqg.DeviceWeights.quantize(torch.randn(256, 512, device="cuda") * 0.02, 128)
+    q, ts = lqg.quantize_activations(torch.randn(8, 512, device="cuda"))
+    with pytest.raises(lqg.ValidationError):
+        dw.gemm(q, ts.cpu())
+    with pytest.raises(lqg.ValidationError):
+        dw.gemm(q, ts.double())
+    with pytest.raises(lqg.ValidationError):
+        dw.gemm(q, ts[:4])
+    with pytest.raises(lqg.ValidationError):
+        dw.gemm(q, ts, out=torch.empty(4, 256, dtype=torch.bfloat16, device="cuda"))
+    with pytest.raises(lqg.ValidationError):
+        dw.gemm(q, ts, out=torch.empty(8, 256, dtype=torch.int8, device="cuda"))
+    with pytest.raises(lqg.ValidationError):
+        dw.gemm_accum(q, out=torch.empty(8, 256, dtype=torch.float32, device="cuda"))
+    torch.cuda.synchronize()
+    assert torch.equal(dw.gemm(q, ts), dw.gemm(q, ts))
+
+
+def test_bundle_mutation_is_seen_by_the_mirror(torch_cuda, lqg, port):
+    """The reference re-reads the bundle on every call; so does the mirror:
+    changing a bundle's arrays after a GEMM changes the next GEMM's result."""
+    rng = np.random.default_rng(9)
+    n, k = 128, 256
+    b = port.build_bundle_plain(make_weights(rng, n, k), 128)
+    bundle = lqg.QuantizedWeightBundle(n, k, 128, lqg.WeightLayout.PlainRowMajor, lqg.FragmentDescriptor(),
+                                       b["packed"].copy(), b["scales"].copy(), b["offsets"].copy(),
+                                       b["channel_scales"].copy())
+    q, ts = port.quantize_activations(make_acts(rng, 4, k))
+    act = lqg.ActivationQuant(4, k, q.reshape(-1), ts)
+    y1 = lqg.gemm_w4a8(act, bundle)
+    bundle.channel_scales = bundle.channel_scales * 2
+    y2 = lqg.gemm_w4a8(act, bundle)
+    b2 = dict(b, channel_scales=bundle.channel_scales)
+    _, y_ref = port.gemm_oracle(q, ts, port.bundle_int8(b2), b2["channel_scales"])
+    np.testing.assert_array_equal(y2.reshape(4, n).view(np.uint32), y_ref.view(np.uint32))
+    assert not np.array_equal(y1, y2)
+
+
 def test_linearity_determinism_and_split_k(torch_cuda, lqg):
     """Size-independent properties at full scale: doubling the activation codes
     doubles the accumulators exactly (test_gemm.cpp:152-172); repeated launches

@@ -34,6 +34,17 @@ def test_file_verdicts_match_reference(lqg, name):
         assert got == msg
 
 
+@pytest.mark.parametrize("name", [n for n, (c, _) in sorted(EXPECTED.items()) if c == 3 and n != "missing.lqwb"])
+def test_truncated_files_raise_ioerror_with_offset(lqg, name):
+    """The Python mirror raises lq::IoError with the reference's message and
+    byte offset (errors.hpp:23-28), the suffix appearing once."""
+    _, msg = EXPECTED[name]
+    with pytest.raises(lqg.IoError) as ei:
+        lqg.DeviceWeights.load(os.path.join(GOLD, name))
+    assert str(ei.value) == msg
+    assert ei.value.byte_offset == int(msg.rsplit(" ", 1)[1].rstrip(")"))
+
+
 def test_load_without_gpu_fails_loudly(lqg):
     """A valid file still needs an sm_100 device to become a handle."""
     import torch

@@ -86,3 +86,59 @@ def test_shard_rows_alignment():
         assert all(s % 128 == 0 for s, _ in r)
     assert shard_rows(8192, 8)[1] == (1024, 2048)
     assert shard_rows(28672, 8)[1] == (3584, 7168)
+
+
+def _p2p_worker(rank, world, port_no, bufs, n, m, calls, out_q):
+    """One rank of the fused (p2p) all-gather protocol over process-shared CPU
+    buffers standing in for NVLink symmetric memory: rank 1 is slow to copy
+    its result out, rank 0 races ahead into the next call's fan-out."""
+    import time
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_no))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2509_01229_b200 import tp
+        layer = tp.ColumnParallelW4A8(n, 64, 64, rank, world)
+        s, e = layer.plan.rows
+
+        def y_of(call):
+            return (torch.arange(m * n, dtype=torch.float32).view(m, n) * (call + 1)) % 251
+
+        def fanout(xq, ts, dests):
+            call = int(xq[0, 0])
+            for d in dests:  # this rank's column slice into every rank's buffer
+                d.copy_(y_of(call)[:, s:e])
+
+        def barrier():
+            dist.barrier()
+            if rank == 1:
+                time.sleep(0.02)  # slow consumer: copy-out lags the peer's next fan-out
+
+        layer.inject_symmetric([(bufs[slot][rank], [bufs[slot][r] for r in range(world)]) for slot in range(2)],
+                               barrier, fanout)
+        ok = True
+        for call in range(calls):
+            xq = torch.full((m, 64), call, dtype=torch.int8)
+            y = layer(xq, torch.ones(m), out_dtype=torch.float32)
+            ok &= bool(torch.equal(y, y_of(call)))
+        out_q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_p2p_gather_double_buffer_has_no_write_after_read_race():
+    """The fused all-gather writes call t into buffer t % 2 of every rank and
+    copies out after a barrier; a fast rank's fan-out of call t + 1 must not
+    clobber a slow rank's unread result of call t (tp.py forward)."""
+    world, n, m, calls = 2, 256, 8, 6
+    bufs = [[torch.zeros(m, n).share_memory_() for _ in range(world)] for _ in range(2)]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port_no = _free_port()
+    procs = [ctx.Process(target=_p2p_worker, args=(r, world, port_no, bufs, n, m, calls, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = sorted(q.get(timeout=180) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok for _, ok in results), results
