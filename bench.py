@@ -645,12 +645,13 @@ def run_7b(lqg, dev, peaks, torch):
         # single launch: one eager GEMM (down), host launch overhead included
         L = layers[3]
         q, ts = xs[L["k"]]
+        qm, tsm, ym, dw0 = q[:m], ts[:m], L["y"][:m], L["dws"][0]
         single = []
         for _ in range(9):
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            L["dws"][0].gemm(q[:m], ts[:m], out=L["y"][:m], workspace=ws)
+            dw0.gemm(qm, tsm, out=ym, workspace=ws)
             e1.record()
             torch.cuda.synchronize()
             single.append(e0.elapsed_time(e1) * 1e3)

@@ -353,6 +353,10 @@ constexpr uint32_t kDecodeWStages = 6;  // W ring depth for token tiles <= 32
 constexpr uint32_t kMaxGroups = 64;  // experts per grouped launch
 // Dynamic shared memory: the two rings, then barriers / schedule / token scales.
 constexpr uint32_t kSmemMax = 227 * 1024;
+// Co-resident kernel: two CTAs (of consecutive launches) per SM, each with
+// 1 KB of driver-reserved shared memory next to its own: 2 x (112 + 1) KB
+// <= 228 KB per SM.
+constexpr uint32_t kSmemMaxCo = 112 * 1024;
 constexpr uint32_t kSmemMisc = 4096;  // 1024-byte alignment pad + barriers + misc (< 3 KB)
 
 // Launch-schedule knobs: token-tile cap, CTA-pair policy, ring split, grid.
@@ -361,7 +365,7 @@ constexpr uint32_t kSmemMisc = 4096;  // 1024-byte alignment pad + barriers + mi
 // tests change them through lqg_tune_set (process-wide, no environment reads).
 enum TuneId : int {
     kTuneMaxBN, kTunePairMinM, kTunePair, kTunePairSingleTile, kTuneXRingBytes, kTuneMaxXStages,
-    kTuneMaxWStages, kTuneGrid, kTuneRasterGM, kTuneNoDP, kTuneNoPDL, kTuneCount
+    kTuneMaxWStages, kTuneGrid, kTuneRasterGM, kTuneNoDP, kTuneNoPDL, kTuneCo, kTuneCount
 };
 struct TuneDef {
     const char* name;
@@ -379,16 +383,17 @@ constexpr TuneDef kTuneDefs[kTuneCount] = {
     {"raster_gm", 0, 0, 1 << 20},                  // 0 = derived
     {"no_dp", 0, 0, 1},                            // stream-K over all tiles
     {"no_pdl", 0, 0, 1},                           // no programmatic dependent launch
+    {"co", 0, 0, 1},                               // co-resident kernel for token tiles <= 32 (measured slower: off)
 };
 std::atomic<int64_t> g_tune[kTuneCount] = {
     {kTuneDefs[0].dflt}, {kTuneDefs[1].dflt}, {kTuneDefs[2].dflt}, {kTuneDefs[3].dflt},
     {kTuneDefs[4].dflt}, {kTuneDefs[5].dflt}, {kTuneDefs[6].dflt}, {kTuneDefs[7].dflt},
-    {kTuneDefs[8].dflt}, {kTuneDefs[9].dflt}, {kTuneDefs[10].dflt}};
+    {kTuneDefs[8].dflt}, {kTuneDefs[9].dflt}, {kTuneDefs[10].dflt}, {kTuneDefs[11].dflt}};
 
 struct Knobs {
     uint32_t max_bn, pair_min_m;
     int pair;
-    uint32_t pair_single_tile, x_ring_bytes, max_x_stages, max_w_stages, grid, raster_gm, no_dp, no_pdl;
+    uint32_t pair_single_tile, x_ring_bytes, max_x_stages, max_w_stages, grid, raster_gm, no_dp, no_pdl, co;
 };
 Knobs knobs() {
     auto g = [](TuneId i) { return g_tune[i].load(std::memory_order_relaxed); };
@@ -404,6 +409,7 @@ Knobs knobs() {
     k.raster_gm = uint32_t(g(kTuneRasterGM));
     k.no_dp = uint32_t(g(kTuneNoDP));
     k.no_pdl = uint32_t(g(kTuneNoPDL));
+    k.co = uint32_t(g(kTuneCo));
     return k;
 }
 
@@ -460,10 +466,17 @@ int activation_tmap(const int8_t* d_x, uint32_t k, uint32_t m, int64_t ldx, uint
     return LQG_OK;
 }
 
-template <uint32_t kG, bool kFan, bool kPair>
+template <uint32_t kG, bool kFan, bool kPair, bool kCo = false>
 int set_smem_attr() {
-    static const cudaError_t e = cudaFuncSetAttribute(lqg_w4a8_gemm_kernel<kG, kFan, kPair>,
-                                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
+    static const cudaError_t e = [] {
+        auto fn = lqg_w4a8_gemm_kernel<kG, kFan, kPair, kCo>;
+        cudaError_t r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             kCo ? kSmemMaxCo : kSmemMax);
+        // the whole unified L1 as shared memory, so two co-resident CTAs fit
+        if (r == cudaSuccess)
+            r = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+        return r;
+    }();
     if (e != cudaSuccess) return set_err(LQG_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
     return LQG_OK;
 }
@@ -536,6 +549,9 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
     const bool pair_legal = n_fan == 0 && (MT > 1 || K.pair_single_tile) && G.NT % 2 == 0 && w->num_sms >= 2;
     const bool pair = pair_legal && (K.pair == 1 || (K.pair == -1 && max_m >= K.pair_min_m));
     if (pair) BN = std::min(kMaxTileM, (BN + 31) / 32 * 32);
+    // Small token tiles run the co-resident kernel (half an SM per CTA), so
+    // consecutive GEMMs in a stream overlap their ramp and tail under PDL.
+    const bool co = !pair && n_fan == 0 && BN <= kSentinelMaxChunks * 16 && K.co;
     CUtensorMap tmap;
     {
         int rc = activation_tmap(d_x, G.k, m, ldx, pair ? BN / 2 : BN, &tmap);
@@ -583,7 +599,7 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
     // X 2 at M = 128). Both rings get the same depth (W even: the dequant
     // warpgroups alternate), X takes any remaining space.
     p.x_slot_bytes = (pair ? BN / 2 : BN) * kKBlock;
-    const uint32_t ring_budget = kSmemMax - kSmemMisc;
+    const uint32_t ring_budget = (co ? kSmemMaxCo : kSmemMax) - kSmemMisc;
     // Decode tiles (<= 32 tokens) keep the W ring at 6: deeper weight
     // prefetch only delays the activation tiles queued behind it (LLaMA-2-70B
     // 4-GEMM step at M = 16: 69 us at 6, 73 us at 10).
@@ -606,7 +622,7 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
     }
     if (sw < 2) return set_err(LQG_EVALIDATION, "tile configuration does not fit shared memory");
     p.w_stages = sw;
-    if (tmem_plan(BN).a_slots < 2)
+    if (tmem_plan(BN, co ? kTmemColsCo : 512u).a_slots < 2)
         return set_err(LQG_EVALIDATION, "tile configuration does not fit tensor memory");
     const uint64_t total_iters = uint64_t(tiles) * G.KB;
     if (total_iters * kMaxSlots >= (uint64_t(1) << 32))
@@ -621,9 +637,12 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
 
     DeviceGuard dg(w->device);
     {
-        int rc = ng > 1 ? (pair ? set_smem_attr<kMaxGroups, false, true>() : set_smem_attr<kMaxGroups, false, false>())
+        int rc = ng > 1 ? (pair ? set_smem_attr<kMaxGroups, false, true>()
+                                : co ? set_smem_attr<kMaxGroups, false, false, true>()
+                                     : set_smem_attr<kMaxGroups, false, false>())
                         : (pair ? set_smem_attr<1, false, true>()
-                                : (n_fan ? set_smem_attr<1, true, false>() : set_smem_attr<1, false, false>()));
+                                : n_fan ? set_smem_attr<1, true, false>()
+                                        : co ? set_smem_attr<1, false, false, true>() : set_smem_attr<1, false, false>());
         if (rc) return rc;
     }
     cudaLaunchConfig_t cfg{};
@@ -657,6 +676,9 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
         uint32_t dp = 0;
         if (T >= units && !K.no_dp) dp = static_cast<uint32_t>(T % units == 0 ? T / units : T / units - 1);
         p.dp_rounds = dp;
+        const uint64_t sk_total = (T - uint64_t(dp) * units) * G.KB;
+        p.sk_q = static_cast<uint32_t>(sk_total / units);
+        p.sk_r = static_cast<uint32_t>(sk_total % units);
         const double ratio = double(units) * ((pair ? 2 : 1) * kTileN / 2.0) / double(BN);
         uint32_t gm = static_cast<uint32_t>(std::lround(std::sqrt(ratio)));
         if (K.raster_gm) gm = K.raster_gm;
@@ -665,6 +687,8 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
     if (ng > 1) {
         if (pair)
             LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<kMaxGroups, false, true>, tmap, p, gt));
+        else if (co)
+            LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<kMaxGroups, false, false, true>, tmap, p, gt));
         else
             LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<kMaxGroups, false, false>, tmap, p, gt));
     } else {
@@ -675,6 +699,8 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
             LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<1, false, true>, tmap, p, g1));
         else if (n_fan)
             LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<1, true, false>, tmap, p, g1));
+        else if (co)
+            LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<1, false, false, true>, tmap, p, g1));
         else
             LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<1, false, false>, tmap, p, g1));
     }

@@ -86,19 +86,23 @@ struct TmemPlan {
     uint32_t acc_stride, acc_stages, a_base, a_slots;
 };
 
-// 512 TMEM columns: double-buffered accumulators whenever two fit next to an
-// A ring of >= 2 slots; the A ring is even (the two dequant warpgroups take
-// alternate k-blocks, so each waits on every other slot and must see every
-// phase of its slots).
-__host__ __device__ inline TmemPlan tmem_plan(uint32_t BN) {
-    constexpr uint32_t cols = 512;
+// TMEM columns per CTA: the whole SM (512), or half of it for the
+// co-resident decode kernel (kCo: two CTAs of consecutive launches share an SM).
+constexpr uint32_t kTmemColsCo = 256;
+
+// Double-buffered accumulators whenever two fit next to an A ring of >= 2
+// slots. Any ring size works with the two dequant warpgroups taking alternate
+// k-blocks: a warpgroup's ring position advances two slots per k-block and
+// flips its parity on every wrap, i.e. parity = (k-block / slots) & 1, the
+// parity of that slot's use count; a slot's next completion needs this
+// warpgroup's own write, so a wait can never be two phases behind.
+__host__ __device__ inline TmemPlan tmem_plan(uint32_t BN, uint32_t cols = 512) {
     TmemPlan t;
     t.acc_stride = (BN + 31) / 32 * 32;
     t.acc_stages = (2 * t.acc_stride + 2 * kACols <= cols) ? 2u : 1u;
     t.a_base = (t.acc_stages * t.acc_stride + kACols - 1) / kACols * kACols;
     t.a_slots = (cols - t.a_base) / kACols;
     if (t.a_slots > kMaxASlots) t.a_slots = kMaxASlots;
-    t.a_slots &= ~1u;
     return t;
 }
 
@@ -127,6 +131,7 @@ struct GemmParams {
                                //    NT/tiles count pair tiles, each CTA owns weight tile 2*nt+rank
                                //    and loads half of every activation tile
     uint32_t tiles;            // weight-tile x token-tile pairs (summed over groups)
+    uint32_t sk_q, sk_r;       // stream-K iterations (tiles after the DP rounds x KB) = sk_q * units + sk_r
 };
 
 // Grouped launch (MoE experts of one layer: same n, k, group size): the
@@ -160,21 +165,25 @@ __device__ __forceinline__ void lqq_dequant_word(uint32_t w, uint32_t s, uint32_
     hi = (((w >> 4) & 0x0F0F0F0Fu) * s + a4) ^ 0x80808080u;
 }
 
-__device__ __forceinline__ uint64_t cta_range_begin(uint32_t c, uint32_t G, uint64_t total) {
-    return total * c / G;
+// First stream-K iteration of unit c: floor(total * c / G) with total =
+// q * G + r (q, r from the host), in 32-bit arithmetic: q * c + r * c / G
+// (r * c < G^2). A 64-bit division is a ~300-cycle subroutine on the GPU and
+// sits on every CTA's prologue.
+__device__ __forceinline__ uint32_t range_begin(uint32_t c, uint32_t G, uint32_t q, uint32_t r) {
+    return q * c + (r * c) / G;
 }
 
 // CTAs whose range starts strictly inside tile `tile` (its contributors):
 // [c_first, c_end). Each contributor's first segment is a piece of the tile.
-__device__ __forceinline__ void split_contributors(uint64_t tile, uint32_t KB, uint32_t G,
-                                                   uint64_t total, uint32_t& c_first,
-                                                   uint32_t& c_end) {
-    const uint64_t t0 = tile * KB, t1 = t0 + KB;
-    uint32_t c = static_cast<uint32_t>(t0 * G / total);
-    while (c > 0 && cta_range_begin(c, G, total) > t0) --c;
-    while (c < G && cta_range_begin(c, G, total) <= t0) ++c;
+__device__ __forceinline__ void split_contributors(uint32_t tile, uint32_t KB, uint32_t G, uint32_t q,
+                                                   uint32_t r, uint32_t& c_first, uint32_t& c_end) {
+    const uint32_t t0 = tile * KB, t1 = t0 + KB;
+    const uint32_t total = q * G + r;
+    uint32_t c = min(G, static_cast<uint32_t>(float(t0) * float(G) / float(total)));
+    while (c > 0 && range_begin(c, G, q, r) > t0) --c;
+    while (c < G && range_begin(c, G, q, r) <= t0) ++c;
     c_first = c;
-    while (c < G && cta_range_begin(c, G, total) < t1) ++c;
+    while (c < G && range_begin(c, G, q, r) < t1) ++c;
     c_end = c;
 }
 
@@ -187,14 +196,10 @@ __device__ __forceinline__ void split_contributors(uint64_t tile, uint32_t KB, u
 // through L2 instead of spanning the whole M x N grid.
 struct Sched {
     uint32_t c, dp_rounds;
-    uint32_t sk_tile0, sk_total, sk_beg, sk_end;  // 32-bit: host guarantees total_iters * G < 2^32
-    uint32_t sk_tile, sk_kb;                      // first stream-K (tile, k-block) of this CTA
+    uint32_t sk_tile0, sk_beg, sk_end;  // 32-bit: host guarantees total_iters * G < 2^32
+    uint32_t sk_tile, sk_kb;            // first stream-K (tile, k-block) of this CTA
     uint32_t n_local;
 };
-
-__device__ __forceinline__ uint32_t range_begin32(uint32_t c, uint32_t G, uint32_t total) {
-    return static_cast<uint32_t>((uint64_t(total) * c) / G);
-}
 
 // Scheduling units: CTAs, or CTA pairs (p.pair).
 __device__ __forceinline__ uint32_t sched_units(const GemmParams& p) {
@@ -207,9 +212,8 @@ __device__ __forceinline__ Sched make_sched(const GemmParams& p) {
     s.c = p.pair ? blockIdx.x >> 1 : blockIdx.x;
     s.dp_rounds = p.dp_rounds;
     s.sk_tile0 = s.dp_rounds * G;
-    s.sk_total = (p.tiles - s.sk_tile0) * p.KB;
-    s.sk_beg = range_begin32(s.c, G, s.sk_total);
-    s.sk_end = range_begin32(s.c + 1, G, s.sk_total);
+    s.sk_beg = range_begin(s.c, G, p.sk_q, p.sk_r);
+    s.sk_end = range_begin(s.c + 1, G, p.sk_q, p.sk_r);
     s.sk_tile = s.sk_tile0 + s.sk_beg / p.KB;
     s.sk_kb = s.sk_beg % p.KB;
     s.n_local = s.dp_rounds * p.KB + (s.sk_end - s.sk_beg);
@@ -324,8 +328,12 @@ __device__ __forceinline__ void store_chunk_k(const GemmParams& p, uint32_t m0, 
         if (kKind == kOutAcc) {
             put(idx, acc[j]);
         } else {
+#ifdef LQG_EXP_FASTEPI  // timing experiment only: FP32 scaling (not bit-exact)
+            const float y = float(acc[j]) * float(cs_d) * float(ts[j]);
+#else
             const double a = i32_to_f64_exact(acc[j]);
             const float y = __double2float_rn(__dmul_rn(__dmul_rn(a, cs_d), ts[j]));
+#endif
             if (kKind == kOutF32)
                 put(idx, y);
             else if (kKind == kOutF16)
@@ -364,7 +372,7 @@ __device__ __forceinline__ void store_chunk(const GemmParams& p, uint32_t m0, ui
 __device__ unsigned long long g_lqg_trace[8 * 160 * 16];
 __device__ __forceinline__ void trace(uint32_t slot, uint32_t e) {
     uint64_t t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");
     g_lqg_trace[(slot * 160 + blockIdx.x) * 16 + e] = t;
 }
 #define LQG_T(e) trace(p.trace_slot, e)
@@ -395,8 +403,16 @@ struct UConst {
 // activation tile (N/2 tokens); the leader issues one M=256 MMA that reads the
 // B halves from both CTAs' shared memory, which halves the activation
 // shared-memory traffic per SM.
-template <uint32_t kG, bool kFan, bool kPair = false>
-__global__ void __launch_bounds__(kThreads, 1)
+// kCo: co-resident launch chain (small token tiles): half an SM per CTA
+// (<= 64 registers per thread, 256 TMEM columns, rings sized by the host to
+// half the shared memory), so under programmatic dependent launch the CTA of
+// the NEXT GEMM in the stream runs on the same SM as this one and streams and
+// dequantizes its first weight chunks (which do not depend on this GEMM)
+// while this one is still in its mainloop and split-K tail. The per-launch
+// ramp (prologue, first DRAM round trip) and tail then overlap instead of
+// adding up across consecutive GEMMs.
+template <uint32_t kG, bool kFan, bool kPair = false, bool kCo = false>
+__global__ void __launch_bounds__(kThreads, kCo ? 2 : 1)
     lqg_w4a8_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const GemmParams p,
                          const __grid_constant__ GroupTable<kG> gt) {
     extern __shared__ uint8_t smem_raw[];
@@ -426,56 +442,72 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const uint32_t G = sched_units(p);
     const uint32_t KB = p.KB;
-    const TmemPlan tp = tmem_plan(p.BN);
+    constexpr uint32_t kTmemCols = kCo ? kTmemColsCo : 512u;
+    const TmemPlan tp = tmem_plan(p.BN, kTmemCols);
     const uint32_t rank = kPair ? ptx::cluster_ctarank() : 0u;  // 0 = pair leader
     // barriers the pair leader waits on, as seen from this CTA
     auto leader = [&](uint32_t bar) { return kPair ? ptx::mapa(bar, 0) : bar; };
 
     if (threadIdx.x == 0) LQG_T(0);
-    if (threadIdx.x == 0) {
-        for (uint32_t s = 0; s < SW; ++s) {
+    if (warp == 0) {
+        // barrier init spread over the lanes of warp 0 (one mbarrier per lane-step)
+        for (uint32_t s = lane; s < SW; s += 32) {
             ptx::mbar_init(wfull_bar(s), 1);
             ptx::mbar_init(wempty_bar(s), 4);  // the 4 warps of the dequant WG of this k-block
         }
-        for (uint32_t s = 0; s < SX; ++s) {
+        for (uint32_t s = lane; s < SX; s += 32) {
             ptx::mbar_init(xfull_bar(s), 1);
             ptx::mbar_init(xempty_bar(s), 1);
         }
-        for (uint32_t a = 0; a < kMaxASlots; ++a) {
-            ptx::mbar_init(afull_bar(a), kPair ? 8 : 4);  // the dequant WG's warps (of both CTAs)
-            ptx::mbar_init(aempty_bar(a), 1);
+        if (lane < kMaxASlots) {
+            ptx::mbar_init(afull_bar(lane), kPair ? 8 : 4);  // the dequant WG's warps (of both CTAs)
+            ptx::mbar_init(aempty_bar(lane), 1);
         }
-        for (uint32_t a = 0; a < 2; ++a) {
-            ptx::mbar_init(accfull_bar(a), 1);
-            ptx::mbar_init(accempty_bar(a), kPair ? 8 : 4);  // one arrive per epilogue warp
+        if (lane < 2) {
+            ptx::mbar_init(accfull_bar(lane), 1);
+            ptx::mbar_init(accempty_bar(lane), kPair ? 8 : 4);  // one arrive per epilogue warp
         }
-        ptx::mbar_init(fin_bar, 1);
+        if (lane == 0) ptx::mbar_init(fin_bar, 1);
         ptx::fence_mbar_init();
     }
     if (warp == kWarpX && lane == 0) ptx::prefetch_tmap(&tmap_x);
     if (warp == kWarpMMA) {
         if (kPair)
-            ptx::tmem_alloc_pair(ptx::smem_u32(tmem_holder), 512);
+            ptx::tmem_alloc_pair(ptx::smem_u32(tmem_holder), kTmemCols);
         else
-            ptx::tmem_alloc(ptx::smem_u32(tmem_holder), 512);
+            ptx::tmem_alloc(ptx::smem_u32(tmem_holder), kTmemCols);
     }
     ptx::tc_fence_before();
     __syncthreads();
+#ifdef LQG_TRACE_PRO
+    if (threadIdx.x == 0) {
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        LQG_TV(3, smid);
+    }
+#endif
     if (kPair) ptx::cluster_sync();  // the peer's barriers are initialised before any remote arrive
     ptx::tc_fence_after();
-    // The CTA owns the SM's whole TMEM (512 columns, one CTA per SM), so the
-    // allocation always starts at lane 0 / column 0: TMEM addresses below are
-    // compile-time offsets (kept in uniform registers by the MMA warp).
-    if (*tmem_holder != 0) __trap();
-    constexpr uint32_t tmem_base = 0;
+    // A full-SM CTA owns all 512 TMEM columns, so its allocation starts at
+    // lane 0 / column 0 and TMEM addresses below are compile-time offsets;
+    // a co-resident CTA owns whichever half it was given.
+    uint32_t tmem_base = 0;
+    if constexpr (kCo) {
+        tmem_base = *tmem_holder;
+    } else {
+        if (*tmem_holder != 0) __trap();
+    }
     // The schedule is recomputed by every thread from kernel parameters and
     // the block index (warp-uniform values, no shared-memory round trip).
     const Sched sch = make_sched(p);
     const uint32_t n_local = sch.n_local;
-    // PDL: let the next kernel in the stream start its prologue and weight
-    // stream now; everything that reads or writes dependent memory below
-    // (activations, token scales, outputs, workspace) sits behind
-    // griddepcontrol.wait.
+    // PDL: the next kernel in the stream may launch now; its CTAs only
+    // prefetch weights until their griddepcontrol.wait, which returns once
+    // this grid has completed and its memory is visible. Everything below
+    // that reads or writes dependent memory (activations, token scales,
+    // outputs, workspace) sits behind griddepcontrol.wait here too. (Issued
+    // after the barrier above: the issuing warp stops counting towards CTA
+    // barriers.)
     if (threadIdx.x == 0) ptx::launch_dependents();
     if (threadIdx.x == 0) LQG_T(1);
 
@@ -621,6 +653,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             a.adv(1, tp.a_slots);
         }
 #ifdef LQG_TRACE
+#ifndef LQG_TRACE_PRO
         if (lane == 0) {  // MMA-warp wait cycles: accumulator, A operand, activation tile, total
             LQG_TV(12, (unsigned long long)w_acc);
             LQG_TV(13, (unsigned long long)w_a);
@@ -628,6 +661,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             LQG_TV(15, (unsigned long long)(clock64() - t_mma0));
             LQG_TV(3, (unsigned long long)w_issue);
         }
+#endif
 #endif
     } else if (warp >= kDequantWarp0 && warp < kEpiWarp0) {
         // ------------------------------------------------------------ dequant WGs
@@ -690,6 +724,45 @@ __global__ void __launch_bounds__(kThreads, 1)
                     prm[2] = t.z;
                     prm[3] = t.w;
                 }
+                const uint32_t a_taddr = a_lane + a.s * kACols;
+                auto dq_param = [&](uint32_t c, uint32_t& sc, uint32_t& a4) {
+                    const uint32_t pi = c / kSubPerP;  // parameter region of sub-block c
+                    const uint32_t sa = (prm[pi / 2] >> (16 * (pi % 2))) & 0xFFFFu;
+                    sc = sa & 0xFFu;
+                    a4 = (sa >> 8) * 0x01010101u;
+                };
+                if constexpr (kCo) {
+                    // Half-SM register budget: a quarter k-block at a time (two
+                    // sub-blocks = 16 words -> 16 TMEM columns), the W slot freed
+                    // once the last quarter's codes are consumed.
+#pragma unroll
+                    for (uint32_t qq = 0; qq < 4; ++qq) {
+                        uint4 v2[2];
+#pragma unroll
+                        for (uint32_t cc = 0; cc < 2; ++cc)
+                            v2[cc] = *reinterpret_cast<const uint4*>(wchunk + ((2 * qq + cc) * kTileN + row) * 16);
+                        if (qq == 0) {
+                            LQG_WAIT(dq_a, ptx::mbar_wait(aempty_bar(a.s), a.ph ^ 1));
+                            ptx::tc_fence_after();
+                        }
+                        int32_t o[16];
+#pragma unroll
+                        for (uint32_t cc = 0; cc < 2; ++cc) {
+                            uint32_t sc, a4;
+                            dq_param(2 * qq + cc, sc, a4);
+                            uint32_t* ou = reinterpret_cast<uint32_t*>(o) + 8 * cc;
+                            lqq_dequant_word(v2[cc].x, sc, a4, ou[0], ou[1]);
+                            lqq_dequant_word(v2[cc].y, sc, a4, ou[2], ou[3]);
+                            lqq_dequant_word(v2[cc].z, sc, a4, ou[4], ou[5]);
+                            lqq_dequant_word(v2[cc].w, sc, a4, ou[6], ou[7]);
+                        }
+                        if (qq == 3) {
+                            __syncwarp();
+                            if (lane == 0) ptx::mbar_arrive(wempty_bar(w.s));
+                        }
+                        ptx::tmem_st_x16(a_taddr + qq * 16, o);
+                    }
+                } else {
                 uint4 v[kSubBlocks];
 #ifdef LQG_EXP_NODQ  // timing experiment only: no code loads (garbage A)
 #pragma unroll
@@ -699,35 +772,30 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (uint32_t c = 0; c < kSubBlocks; ++c)
                     v[c] = *reinterpret_cast<const uint4*>(wchunk + (c * kTileN + row) * 16);
 #endif
+                // The whole k-block is converted before the A slot is claimed, so
+                // once the MMA frees the slot only the two TMEM stores stand
+                // between it and the next afull arrival (two A slots per
+                // warpgroup at the largest token tile: this latency, not the
+                // ALU work, gates the tensor pipe).
+                uint32_t o[2][32];
+#pragma unroll
+                for (uint32_t c = 0; c < kSubBlocks; ++c) {
+                    uint32_t sc, a4;
+                    dq_param(c, sc, a4);
+                    uint32_t* oc = &o[c / 4][8 * (c % 4)];
+                    lqq_dequant_word(v[c].x, sc, a4, oc[0], oc[1]);
+                    lqq_dequant_word(v[c].y, sc, a4, oc[2], oc[3]);
+                    lqq_dequant_word(v[c].z, sc, a4, oc[4], oc[5]);
+                    lqq_dequant_word(v[c].w, sc, a4, oc[6], oc[7]);
+                }
+                // every code of the chunk has been consumed: free the W slot
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(wempty_bar(w.s));
                 LQG_WAIT(dq_a, ptx::mbar_wait(aempty_bar(a.s), a.ph ^ 1));
                 ptx::tc_fence_after();
-                const uint32_t a_taddr = a_lane + a.s * kACols;
-#pragma unroll
-                for (uint32_t h = 0; h < 2; ++h) {
-                    uint32_t o[32];
-#pragma unroll
-                    for (uint32_t cc = 0; cc < 4; ++cc) {
-                        const uint32_t c = 4 * h + cc;
-                        const uint32_t pi = c / kSubPerP;  // parameter region of sub-block c
-                        const uint32_t sa = (prm[pi / 2] >> (16 * (pi % 2))) & 0xFFFFu;
-                        const uint32_t sc = sa & 0xFFu;
-                        const uint32_t a4 = (sa >> 8) * 0x01010101u;
-                        lqq_dequant_word(v[c].x, sc, a4, o[8 * cc + 0], o[8 * cc + 1]);
-                        lqq_dequant_word(v[c].y, sc, a4, o[8 * cc + 2], o[8 * cc + 3]);
-                        lqq_dequant_word(v[c].z, sc, a4, o[8 * cc + 4], o[8 * cc + 5]);
-                        lqq_dequant_word(v[c].w, sc, a4, o[8 * cc + 6], o[8 * cc + 7]);
-                    }
-                    if (h == 1) {
-                        // every code of the chunk has been consumed: free the W slot
-                        __syncwarp();
-                        if (lane == 0) ptx::mbar_arrive(wempty_bar(w.s));
-                    }
-#ifdef LQG_EXP_NOSTTM  // timing experiment only: A never written (garbage A)
-                    if (o[0] == 0x12345678u && o[31] == 0x9abcdef0u) ptx::tmem_st_x32(a_taddr + h * 32, o);
-#else
-                    ptx::tmem_st_x32(a_taddr + h * 32, o);
-#endif
-                }
+                ptx::tmem_st_x32(a_taddr, o[0]);
+                ptx::tmem_st_x32(a_taddr + 32, o[1]);
+                }  // !kCo
                 ptx::tmem_st_wait();
                 ptx::tc_fence_before();
                 wait_x();
@@ -741,7 +809,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 w.adv(2, SW);
                 a.adv(2, tp.a_slots);
             }
-#ifdef LQG_TRACE
+#if defined(LQG_TRACE) && !defined(LQG_TRACE_PRO)
             if (warp == kDequantWarp0 && lane == 0) {  // dequant waits: weights, A slot, total
                 LQG_TV(11, (unsigned long long)(clock64() - t_dq0));
                 LQG_TV(9, (unsigned long long)dq_w);
@@ -799,26 +867,28 @@ __global__ void __launch_bounds__(kThreads, 1)
             // segment's MMAs run; for small token tiles also request the first
             // batch's chunk-0 cells (they are usually published by now).
             const bool finisher = n_iters < KB && kb0 == 0;
-            const bool small = nchunks <= kSentinelMaxChunks;
+            // (the co-resident kernel only runs small token tiles)
+            const bool small = kCo || nchunks <= kSentinelMaxChunks;
             uint32_t c_first = 0, c_end = 0;
-            // Split-K cells of up to four contributors for one 16-token chunk:
+            // Split-K cells of up to kCB contributors for one 16-token chunk:
             // [contributor][quad]. Loaded one chunk ahead (software pipeline).
-            int4 cb[4][4];
+            constexpr uint32_t kCB = kCo ? 1u : 4u;  // contributors per L2 round trip
+            int4 cb[kCB][4];
             auto cell_of = [&](uint32_t c, uint32_t ch) {
                 const uint32_t cs_slot = kPair ? 2 * c + rank : c;  // the matching CTA of a contributor pair
                 return reinterpret_cast<int4*>(p.parts + uint64_t(cs_slot) * kSlotCellsK + (small ? 0u : kSmallCells)) +
                        ch * 4 * kTileN + row;
             };
             auto load_batch = [&](uint32_t c, uint32_t ch) {
-                const uint32_t nb = min(4u, c_end - c);
+                const uint32_t nb = min(kCB, c_end - c);
 #pragma unroll
-                for (uint32_t b = 0; b < 4; ++b)
+                for (uint32_t b = 0; b < kCB; ++b)
                     if (b < nb)
 #pragma unroll
                         for (uint32_t q = 0; q < 4; ++q) cb[b][q] = __ldcg(cell_of(c + b, ch) + q * kTileN);
             };
             if (finisher) {
-                split_contributors(uint64_t(tile - sch.sk_tile0), KB, G, sch.sk_total, c_first, c_end);
+                split_contributors(tile - sch.sk_tile0, KB, G, p.sk_q, p.sk_r, c_first, c_end);
                 if (small) load_batch(c_first, 0);
             }
             asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -871,7 +941,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         __stcg(cell + q * kTileN, make_int4(int32_t(v[4 * q]), int32_t(v[4 * q + 1]),
                                                             int32_t(v[4 * q + 2]), int32_t(v[4 * q + 3])));
                 }
-                if (nchunks > kSentinelMaxChunks) {
+                if (!small) {
                     // large tiles: every epilogue thread's stores, then one release flag
                     __threadfence();
                     asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -897,8 +967,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                         int32_t sum[16];
 #pragma unroll
                         for (uint32_t j = 0; j < 16; ++j) sum[j] = int32_t(v[j]);
-                        for (uint32_t c = c_first; c < c_end; c += 4) {
-                            const uint32_t nb = min(4u, c_end - c);
+                        for (uint32_t c = c_first; c < c_end; c += kCB) {
+                            const uint32_t nb = min(kCB, c_end - c);
                             if (c != c_first) load_batch(c, ch);
                             auto pend = [](const int4& x) {
                                 return x.x == INT32_MIN || x.y == INT32_MIN || x.z == INT32_MIN ||
@@ -907,21 +977,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                             for (;;) {
                                 uint32_t mask = 0;
 #pragma unroll
-                                for (uint32_t b = 0; b < 4; ++b)
+                                for (uint32_t b = 0; b < kCB; ++b)
 #pragma unroll
                                     for (uint32_t q = 0; q < 4; ++q)
                                         mask |= (b < nb && pend(cb[b][q])) ? (1u << (4 * b + q)) : 0u;
                                 if (!mask) break;
                                 __nanosleep(32);
 #pragma unroll
-                                for (uint32_t b = 0; b < 4; ++b)
+                                for (uint32_t b = 0; b < kCB; ++b)
 #pragma unroll
                                     for (uint32_t q = 0; q < 4; ++q)
                                         if (mask & (1u << (4 * b + q)))
                                             cb[b][q] = ptx::ld_relaxed_v4(cell_of(c + b, ch) + q * kTileN);
                             }
 #pragma unroll
-                            for (uint32_t b = 0; b < 4; ++b) {
+                            for (uint32_t b = 0; b < kCB; ++b) {
                                 if (b < nb) {
 #pragma unroll
                                     for (uint32_t q = 0; q < 4; ++q) {
@@ -934,7 +1004,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                     }
                                 }
                             }
-                            if (c + 4 >= c_end && ch + 1 < nchunks) load_batch(c_first, ch + 1);
+                            if (c + kCB >= c_end && ch + 1 < nchunks) load_batch(c_first, ch + 1);
                         }
                         if (n < p.N) store_chunk<kFan>(p, m0 + ch * 16, mlim, n, sum, cs, ts_s + ch * 16);
                     }
@@ -950,12 +1020,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t part_bytes = p.BN * kTileN * 4;
                     const uint32_t nb_max = max(1u, ring_bytes / part_bytes);
                     const int4* sm4 = reinterpret_cast<const int4*>(smem);
+#ifdef LQG_TRACE_PRO
+                    if (et == 0) LQG_T(9);
+#endif
                     for (uint32_t c = c_first + et; c < c_end; c += 128) {
                         const uint32_t fc = kPair ? 2 * c + rank : c;
                         while (ptx::ld_acquire_u32(p.flags + fc) == 0) __nanosleep(32);
                         p.flags[fc] = 0;
                     }
                     asm volatile("bar.sync 1, 128;" ::: "memory");
+#ifdef LQG_TRACE_PRO
+                    if (et == 0) LQG_T(10);
+#endif
                     for (uint32_t c0 = c_first; c0 < c_end; c0 += nb_max) {
                         const uint32_t nb = min(nb_max, c_end - c0);
                         const bool last_batch = c0 + nb >= c_end;
@@ -969,6 +1045,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                         ptx::mbar_wait(fin_bar, fin_ph);
                         fin_ph ^= 1;
+#ifdef LQG_TRACE_PRO
+                        if (et == 0) LQG_T(11);
+#endif
                         for (uint32_t ch = 0; ch < nchunks; ++ch) {
                             uint32_t v[16];
                             ptx::tmem_ld_x16(acc_taddr + ch * 16, v);
@@ -980,7 +1059,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 const int4* scell = sm4 + b * (part_bytes / 16) + ch * 4 * kTileN + row;
 #pragma unroll
                                 for (uint32_t q = 0; q < 4; ++q) {
+#ifdef LQG_EXP_NOFINSUM  // timing experiment only: partials not read back
+                                    const int4 x = make_int4(q, b, ch, 0);
+#else
                                     const int4 x = scell[q * kTileN];
+#endif
                                     sum[4 * q] += x.x;
                                     sum[4 * q + 1] += x.y;
                                     sum[4 * q + 2] += x.z;
@@ -992,28 +1075,45 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 ptx::tmem_st_x16(acc_taddr + ch * 16, sum);
                             } else {
                                 if (ch == 0 && et == 0) LQG_T(8);
-                                if (n < p.N) store_chunk<kFan>(p, m0 + ch * 16, mlim, n, sum, cs, ts_s + ch * 16);
+#ifdef LQG_EXP_NOFINSTORE  // timing experiment only: no final stores
+                                if (n < p.N && sum[0] == 0x7fffffff && sum[15] == 0x7ffffffe)
+#else
+                                if (n < p.N)
+#endif
+                                    store_chunk<kFan>(p, m0 + ch * 16, mlim, n, sum, cs, ts_s + ch * 16);
+#ifdef LQG_TRACE_PRO
+                                if (ch == 0 && et == 0) LQG_T(15);
+#endif
                             }
                         }
                         if (!last_batch) ptx::tmem_st_wait();
                         asm volatile("bar.sync 1, 128;" ::: "memory");  // ring reads done before the next batch
                     }
+#ifdef LQG_TRACE_PRO
+                    if (et == 0) LQG_T(14);
+#endif
                 }
                 release_acc(cur_as);
             }
             asm volatile("bar.sync 1, 128;" ::: "memory");  // ts_s reuse
         }
+#ifdef LQG_TRACE_PRO
+        if (et == 0) LQG_T(13);
+#endif
     }
 
     ptx::tc_fence_before();
     __syncthreads();
+#ifdef LQG_TRACE_PRO
+    if (threadIdx.x == 0) LQG_T(12);
+#endif
     ptx::tc_fence_after();
     if (kPair) ptx::cluster_sync();  // the leader's MMAs into this CTA's TMEM are complete
     if (warp == kWarpMMA) {
         if (kPair)
-            ptx::tmem_dealloc_pair(tmem_base, 512);
+            ptx::tmem_dealloc_pair(tmem_base, kTmemCols);
         else
-            ptx::tmem_dealloc(tmem_base, 512);
+            ptx::tmem_dealloc(tmem_base, kTmemCols);
     }
 }
 

@@ -278,10 +278,28 @@ def _y_code(dtype) -> int:
     return Y_DTYPES[name]
 
 
-def _stream_ptr(stream):
-    import torch
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return C.c_void_p(s.cuda_stream)
+_TORCH = None
+
+
+def _torch():
+    """torch and the dtype objects the launch path compares against, imported
+    once (the eager launch path is a few microseconds of host time)."""
+    global _TORCH
+    if _TORCH is None:
+        import torch
+        _TORCH = (torch, torch.int8, torch.float32, torch.int32,
+                  {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2})
+    return _TORCH
+
+
+def _stream_ptr(stream, device: int | None = None):
+    """Raw cudaStream_t of `stream`, or of the current stream of `device`."""
+    torch = _torch()[0]
+    if stream is not None:
+        return C.c_void_p(stream.cuda_stream)
+    if device is None:
+        device = torch.cuda.current_device()
+    return C.c_void_p(torch._C._cuda_getCurrentRawStream(device))
 
 
 class Workspace:
@@ -364,23 +382,24 @@ class DeviceWeights:
         return int(_lib.lib().lqg_weights_device_bytes(self.handle))
 
     def _check_x(self, xq):
-        import torch
-        if not (xq.is_cuda and xq.dtype == torch.int8 and xq.dim() == 2 and xq.shape[1] == self.k
+        torch, i8 = _torch()[:2]
+        if not (xq.dtype is i8 and xq.is_cuda and xq.dim() == 2 and xq.shape[1] == self.k
                 and xq.stride(1) == 1):
             raise ValidationError(f"activations must be a CUDA int8 [m, {self.k}] row-major tensor")
-        if xq.device.index != self.device:
-            raise ValidationError(f"activations live on cuda:{xq.device.index}, weights on cuda:{self.device}")
+        if xq.get_device() != self.device:
+            raise ValidationError(f"activations live on cuda:{xq.get_device()}, weights on cuda:{self.device}")
 
     def _check_ts(self, ts, m):
-        import torch
-        if not (ts.is_cuda and ts.dtype == torch.float32 and ts.dim() == 1 and ts.stride(0) == 1
-                and ts.shape[0] >= m and ts.device.index == self.device):
+        f32 = _torch()[2]
+        if not (ts.dtype is f32 and ts.is_cuda and ts.dim() == 1 and ts.stride(0) == 1
+                and ts.shape[0] >= m and ts.get_device() == self.device):
             raise ValidationError(f"token scales must be a contiguous CUDA float32 [>= {m}] tensor "
                                   f"on cuda:{self.device}")
 
     def _check_out(self, out, m, dtypes):
-        if not (out.is_cuda and out.device.index == self.device and out.dim() == 2
-                and tuple(out.shape) == (m, self.n) and out.stride(1) == 1 and out.stride(0) >= self.n):
+        if not (out.is_cuda and out.get_device() == self.device and out.dim() == 2
+                and out.shape[0] == m and out.shape[1] == self.n and out.stride(1) == 1
+                and out.stride(0) >= self.n):
             raise ValidationError(f"output must be a row-major CUDA [{m}, {self.n}] tensor on cuda:{self.device}")
         if str(out.dtype).replace("torch.", "") not in dtypes:
             raise ValidationError(f"unsupported output dtype {out.dtype}")
@@ -388,17 +407,23 @@ class DeviceWeights:
     def gemm(self, xq, ts, out=None, out_dtype=None, workspace: Workspace | None = None,
              stream=None):
         """Y[m, n] = (X_i8 @ W^_i8.T) * cs[n] * ts[m] in out_dtype (default bf16)."""
-        import torch
+        torch, _, _, _, ycodes = _torch()
         self._check_x(xq)
         m = xq.shape[0]
         self._check_ts(ts, m)
         if out is None:
             out = torch.empty(m, self.n, dtype=out_dtype or torch.bfloat16, device=xq.device)
-        self._check_out(out, m, Y_DTYPES)
+        elif not (out.is_cuda and out.get_device() == self.device and out.dim() == 2
+                  and out.shape[0] == m and out.shape[1] == self.n and out.stride(1) == 1
+                  and out.stride(0) >= self.n):
+            raise ValidationError(f"output must be a row-major CUDA [{m}, {self.n}] tensor on cuda:{self.device}")
+        code = ycodes.get(out.dtype)
+        if code is None:
+            raise ValidationError(f"unsupported output dtype {out.dtype}")
         check(_lib.lib().lqg_gemm_w4a8(
             self.handle, xq.data_ptr(), xq.stride(0), ts.data_ptr(), m, out.data_ptr(),
-            out.stride(0), _y_code(out.dtype), workspace.handle if workspace else None,
-            _stream_ptr(stream)))
+            out.stride(0), code, workspace.handle if workspace else None,
+            _stream_ptr(stream, self.device)))
         return out
 
     def gemm_fanout(self, xq, ts, outs, workspace: Workspace | None = None, stream=None):
@@ -418,7 +443,7 @@ class DeviceWeights:
         ptrs = (C.c_void_p * len(outs))(*[o.data_ptr() for o in outs])
         check(_lib.lib().lqg_gemm_w4a8_fanout(
             self.handle, xq.data_ptr(), xq.stride(0), ts.data_ptr(), m, ptrs, len(outs), ld,
-            _y_code(outs[0].dtype), workspace.handle if workspace else None, _stream_ptr(stream)))
+            _y_code(outs[0].dtype), workspace.handle if workspace else None, _stream_ptr(stream, self.device)))
         return outs[0]
 
     def gemm_accum(self, xq, out=None, workspace: Workspace | None = None, stream=None):
@@ -430,7 +455,7 @@ class DeviceWeights:
         self._check_out(out, m, ("int32",))
         check(_lib.lib().lqg_gemm_w4a8_accum(
             self.handle, xq.data_ptr(), xq.stride(0), m, out.data_ptr(), out.stride(0),
-            workspace.handle if workspace else None, _stream_ptr(stream)))
+            workspace.handle if workspace else None, _stream_ptr(stream, self.device)))
         return out
 
     def gemm_host(self, x_host, ts_host, y_host, stream=None) -> None:
@@ -440,7 +465,7 @@ class DeviceWeights:
         m = x_host.shape[0]
         check(_lib.lib().lqg_gemm_w4a8_host(self.handle, x_host.data_ptr(), ts_host.data_ptr(), m,
                                             y_host.data_ptr(), _y_code(y_host.dtype),
-                                            _stream_ptr(stream)))
+                                            _stream_ptr(stream, self.device)))
 
     def dequant(self, out=None, stream=None):
         """W^ as INT8 [n, k] through the mainloop's LQQ routine."""
@@ -448,7 +473,7 @@ class DeviceWeights:
         if out is None:
             out = torch.empty(self.n, self.k, dtype=torch.int8, device=f"cuda:{self.device}")
         check(_lib.lib().lqg_dequant_weights(self.handle, out.data_ptr(), out.stride(0),
-                                             _stream_ptr(stream)))
+                                             _stream_ptr(stream, self.device)))
         return out
 
     def export(self) -> QuantizedWeightBundle:
@@ -503,7 +528,7 @@ def gemm_grouped(weights, xq, ts, m_list, out=None, out_dtype=None,
     check(_lib.lib().lqg_gemm_w4a8_grouped(
         handles, len(weights), xq.data_ptr(), xq.stride(0), ts.data_ptr(), ms.ctypes.data,
         out.data_ptr(), out.stride(0), _y_code(out.dtype), workspace.handle if workspace else None,
-        _stream_ptr(stream)))
+        _stream_ptr(stream, xq.get_device())))
     return out
 
 
@@ -516,7 +541,7 @@ def gemm_grouped_accum(weights, xq, m_list, out=None, workspace: Workspace | Non
         out = torch.empty(xq.shape[0], weights[0].n, dtype=torch.int32, device=xq.device)
     check(_lib.lib().lqg_gemm_w4a8_grouped_accum(
         handles, len(weights), xq.data_ptr(), xq.stride(0), ms.ctypes.data, out.data_ptr(),
-        out.stride(0), workspace.handle if workspace else None, _stream_ptr(stream)))
+        out.stride(0), workspace.handle if workspace else None, _stream_ptr(stream, xq.get_device())))
     return out
 
 
@@ -531,7 +556,7 @@ def quantize_activations(x, out_q=None, out_ts=None, check_finite: bool = False,
     ts = out_ts if out_ts is not None else torch.empty(m, dtype=torch.float32, device=x.device)
     check(_lib.lib().lqg_quantize_activations(x.data_ptr(), x.stride(0), m, k, q.data_ptr(),
                                               q.stride(0), ts.data_ptr(), int(check_finite),
-                                              _stream_ptr(stream)))
+                                              _stream_ptr(stream, x.get_device())))
     return q, ts
 
 

@@ -618,7 +618,8 @@ def test_pair_threshold_boundary_is_seamless(torch_cuda, lqg):
                                    (200, 256, 8192), (700, 512, 1536)])
 @pytest.mark.parametrize("knobs", [dict(max_w_stages=2), dict(max_w_stages=4, x_ring_bytes=1024),
                                    dict(max_x_stages=2, x_ring_bytes=1024), dict(grid=7), dict(grid=64, no_dp=1),
-                                   dict(max_bn=32), dict(pair=1, pair_single_tile=1), dict(no_pdl=1)])
+                                   dict(max_bn=32), dict(pair=1, pair_single_tile=1), dict(no_pdl=1),
+                                   dict(co=1)])
 def test_schedule_knobs_bit_exact(torch_cuda, lqg, m, n, k, knobs):
     """Every ring split (2-stage W ring, minimal X ring), grid size, token
     tile and pair policy gives the same INT32 accumulators and BF16 outputs as
@@ -633,6 +634,41 @@ def test_schedule_knobs_bit_exact(torch_cuda, lqg, m, n, k, knobs):
         acc1, y1 = dw.gemm_accum(q), dw.gemm(q, ts)
     torch.cuda.synchronize()
     assert torch.equal(acc0, acc1) and torch.equal(y0, y1)
+
+
+@pytest.mark.parametrize("m", [1, 16, 32])
+def test_coresident_launch_chain(torch_cuda, lqg, m):
+    """Back-to-back decode GEMMs on one stream with the co-resident kernel
+    (tune co=1): the next launch's CTAs share SMs with the previous launch and
+    prefill their weight rings before griddepcontrol.wait. A chain over
+    alternating weights, shapes and output kinds with a shared split-K
+    workspace is bit-identical to the same launches with full-SM CTAs (the
+    default, tune co=0)."""
+    torch = torch_cuda
+    g = torch.Generator(device="cuda").manual_seed(77 + m)
+    shapes = [(4096, 4096), (1024, 11008), (12288, 4096), (4096, 4096)]
+    dws = [lqg.DeviceWeights.quantize(torch.randn(n, k, generator=g, device="cuda") * 0.02, 128)
+           for n, k in shapes]
+    xs = {k: lqg.quantize_activations(torch.randn(m, k, generator=g, device="cuda")) for _, k in shapes}
+    ws = lqg.Workspace(0)
+
+    def chain():
+        outs = []
+        for rep in range(3):
+            for i, dw in enumerate(dws):
+                q, ts = xs[dw.k]
+                if (i + rep) % 3 == 0:
+                    outs.append(dw.gemm_accum(q, workspace=ws))
+                else:
+                    outs.append(dw.gemm(q, ts, out_dtype=torch.bfloat16 if i % 2 else torch.float32,
+                                        workspace=ws))
+        torch.cuda.synchronize()
+        return outs
+    ref = chain()
+    for _ in range(3):
+        got = _with_tune(lqg, chain, co=1)
+        for a, b in zip(ref, got):
+            assert torch.equal(a, b)
 
 
 def test_tune_rejects_unknown_and_out_of_range(lqg):

@@ -1,5 +1,7 @@
-"""A/B timing of liblqg variants in one process per variant, alternated:
+"""A/B timing of liblqg variants (or schedule knob sets) in one process per
+variant, alternated:
   python tools/ab.py --libs a.so,b.so --ms 16 --rounds 3
+  python tools/ab.py --libs a.so --tunes "max_bn=192;max_bn=160" --ms 1024,4096
 Times the 70B 4-layer step at each M as a CUDA graph (3 rotations), like bench.py."""
 import argparse, json, os, subprocess, sys
 
@@ -9,6 +11,9 @@ import os, sys, json, time
 sys.path.insert(0, ROOT)
 import torch
 import paper_2509_01229_b200 as lqg
+for kv in filter(None, TUNE.split(",")):
+    kk, vv = kv.split("=")
+    lqg.tune_set(kk, int(vv))
 shapes = [(10240, 8192), (8192, 8192), (28672, 8192), (8192, 28672)]
 ms = MS
 g = torch.Generator(device="cuda"); g.manual_seed(1)
@@ -44,8 +49,14 @@ def main():
     ap.add_argument("--rounds", type=int, default=3)
     ap.add_argument("--idle", type=float, default=1.5, help="seconds idle before each timing")
     ap.add_argument("--env", default="", help="extra env per lib, ';'-separated list of k=v,k=v")
+    ap.add_argument("--tunes", default="", help="';'-separated knob sets k=v,k=v (one variant each)")
     a = ap.parse_args()
     libs = a.libs.split(",")
+    tunes = a.tunes.split(";") if a.tunes else [""]
+    if len(libs) == 1 and len(tunes) > 1:
+        libs = libs * len(tunes)
+    if len(tunes) == 1:
+        tunes = tunes * len(libs)
     envs = a.env.split(";") if a.env else [""] * len(libs)
     ms = [int(x) for x in a.ms.split(",")]
     res = {i: [] for i in range(len(libs))}
@@ -55,7 +66,8 @@ def main():
             for kv in filter(None, envs[i].split(",")):
                 k, v = kv.split("=")
                 env[k] = v
-            code = CHILD.replace("ROOT", repr(ROOT)).replace("MS", repr(ms)).replace("IDLE", repr(a.idle))
+            code = (CHILD.replace("ROOT", repr(ROOT)).replace("MS", repr(ms)).replace("IDLE", repr(a.idle))
+                    .replace("TUNE", repr(tunes[i])))
             o = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
             if o.returncode:
                 print(lib, "FAILED", o.stderr[-500:]); continue
@@ -63,7 +75,7 @@ def main():
     for i, lib in enumerate(libs):
         for m in ms:
             v = [x[str(m)] for x in res[i]]
-            print(f"{os.path.basename(lib):28s} {envs[i]:30s} M={m:5d}: " + " ".join(f"{t:7.1f}" for t in v) + f"  min {min(v):.1f} us")
+            print(f"{os.path.basename(lib):20s} {envs[i] + tunes[i]:30s} M={m:5d}: " + " ".join(f"{t:7.1f}" for t in v) + f"  min {min(v):.1f} us")
 
 if __name__ == "__main__":
     main()

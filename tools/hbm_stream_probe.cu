@@ -114,6 +114,20 @@ int main() {
         float ms = timeit([&] { ldg_stream<<<blocks, 512>>>(reinterpret_cast<const uint4*>(buf), bytes / 16, sink); });
         printf("ldg grid=%d x 512: %.1f GB/s\n", blocks, bytes / (ms * 1e-3) / 1e9);
     }
+    // Single-launch streaming floor at the LLaMA-2 layer sizes: R back-to-back
+    // launches, each over its own region of the buffer (no L2 reuse).
+    for (double mb : {8.65, 23.2, 25.9, 34.6, 121.6}) {
+        const uint32_t chunk = 16896, stages = 12;
+        const uint64_t nchunks = uint64_t(mb * 1e6) / chunk;
+        const int R = 12;
+        float ms = timeit([&] {
+            for (int r = 0; r < R; ++r)
+                bulk_stream<<<sms, 256, stages * chunk + 512>>>(buf + r * nchunks * chunk, nchunks, chunk, stages,
+                                                                sink);
+        });
+        printf("single-launch %.2f MB: %.2f us/launch = %.1f GB/s\n", mb, ms * 1e3 / R,
+               nchunks * chunk * R / (ms * 1e-3) / 1e9);
+    }
     cudaError_t err = cudaGetLastError();
     printf("status: %s\n", cudaGetErrorString(err));
     return 0;
