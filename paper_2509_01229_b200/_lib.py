@@ -14,13 +14,15 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB_PATH = os.environ.get("LQG_LIB_PATH") or os.path.join(HERE, "liblqg.so")
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["lqg_api.cu"]
-HEADERS = ["lqg_gemm.cuh", "lqg_aux.cuh", "lqg_layout.h", "sm100_ptx.cuh"]
+SOURCES = ["lqg_api.cu", "lqg_kern.cu"]
+HEADERS = ["lqg_gemm.cuh", "lqg_aux.cuh", "lqg_layout.h", "sm100_ptx.cuh", "lqg_launch.h"]
+# lqg_kern.cu is compiled once per output kind (lqg::OutKind 0..3), in parallel
+KINDS = (0, 1, 2, 3)
 
 NVCC_FLAGS = [
     "-std=c++17", "-O3", "-lineinfo",
     "-gencode", "arch=compute_100a,code=sm_100a",
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC",
 ]
 
 
@@ -33,15 +35,30 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, defines: tuple = (), out: str | None = None) -> str:
-    """Compile liblqg.so for sm_100a (cross-compiles without a GPU). `defines`
-    and `out` build debug variants (e.g. -DLQG_TRACE into liblqg_trace.so)."""
+    """Compile liblqg.so for sm_100a (cross-compiles without a GPU): the host
+    API and the four per-output-kind kernel units are compiled in parallel,
+    then linked. `defines` and `out` build debug variants (e.g. -DLQG_TRACE
+    into liblqg_trace.so)."""
+    import shutil
+    import tempfile
     target = out or LIB_PATH
     if not force and not out and not _stale():
         return LIB_PATH
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, *(["-Xptxas", "-v"] if verbose else []), *[f"-D{d}" for d in defines],
-           "-o", target + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES]]
-    subprocess.run(cmd, check=True)
+    base = [nvcc, *NVCC_FLAGS, *(["-Xptxas", "-v"] if verbose else []), *[f"-D{d}" for d in defines]]
+    tmp = tempfile.mkdtemp(prefix="lqg_build_")
+    try:
+        units = [(os.path.join(CSRC, "lqg_api.cu"), os.path.join(tmp, "api.o"), [])]
+        units += [(os.path.join(CSRC, "lqg_kern.cu"), os.path.join(tmp, f"kern{k}.o"), [f"-DLQG_KIND={k}"])
+                  for k in KINDS]
+        procs = [subprocess.Popen([*base, *extra, "-c", "-o", obj, src]) for src, obj, extra in units]
+        rcs = [pr.wait() for pr in procs]
+        if any(rcs):
+            raise subprocess.CalledProcessError(max(rcs), "nvcc")
+        subprocess.run([nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", target + ".tmp",
+                        *[obj for _, obj, _ in units]], check=True)
+    finally:
+        shutil.rmtree(tmp, ignore_errors=True)
     os.replace(target + ".tmp", target)
     return target
 

@@ -17,7 +17,7 @@
 
 #include "../../include/lqg.h"
 #include "lqg_aux.cuh"
-#include "lqg_gemm.cuh"
+#include "lqg_launch.h"
 #include "lqg_layout.h"
 
 using namespace lqg;
@@ -350,14 +350,10 @@ constexpr uint32_t kMaxTileM = 192;
 // M = 128 117 -> 110 us, M = 256 176 -> 159 us; M = 16 unchanged either way).
 constexpr uint32_t kPairMinM = 48;
 constexpr uint32_t kDecodeWStages = 6;  // W ring depth for token tiles <= 32
-constexpr uint32_t kMaxGroups = 64;  // experts per grouped launch
 // Dynamic shared memory: the two rings, then barriers / schedule / token scales.
-constexpr uint32_t kSmemMax = 227 * 1024;
-// Co-resident kernel: two CTAs (of consecutive launches) per SM, each with
-// 1 KB of driver-reserved shared memory next to its own: 2 x (112 + 1) KB
-// <= 228 KB per SM.
-constexpr uint32_t kSmemMaxCo = 112 * 1024;
-constexpr uint32_t kSmemMisc = 4096;  // 1024-byte alignment pad + barriers + misc (< 3 KB)
+
+// 1024-byte alignment pad + mbarriers + misc (holder, token scales, output staging)
+constexpr uint32_t kSmemMisc = (1024 + 8 * kNumBarriers + 8 + kMiscBytes + 1023) / 1024 * 1024;
 
 // Launch-schedule knobs: token-tile cap, CTA-pair policy, ring split, grid.
 // Results never depend on them (every setting is bit-exact, tested); they
@@ -365,7 +361,7 @@ constexpr uint32_t kSmemMisc = 4096;  // 1024-byte alignment pad + barriers + mi
 // tests change them through lqg_tune_set (process-wide, no environment reads).
 enum TuneId : int {
     kTuneMaxBN, kTunePairMinM, kTunePair, kTunePairSingleTile, kTuneXRingBytes, kTuneMaxXStages,
-    kTuneMaxWStages, kTuneGrid, kTuneRasterGM, kTuneNoDP, kTuneNoPDL, kTuneCo, kTuneCount
+    kTuneMaxWStages, kTuneGrid, kTuneRasterGM, kTuneNoDP, kTuneNoPDL, kTuneCount
 };
 struct TuneDef {
     const char* name;
@@ -383,17 +379,16 @@ constexpr TuneDef kTuneDefs[kTuneCount] = {
     {"raster_gm", 0, 0, 1 << 20},                  // 0 = derived
     {"no_dp", 0, 0, 1},                            // stream-K over all tiles
     {"no_pdl", 0, 0, 1},                           // no programmatic dependent launch
-    {"co", 0, 0, 1},                               // co-resident kernel for token tiles <= 32 (measured slower: off)
 };
 std::atomic<int64_t> g_tune[kTuneCount] = {
     {kTuneDefs[0].dflt}, {kTuneDefs[1].dflt}, {kTuneDefs[2].dflt}, {kTuneDefs[3].dflt},
     {kTuneDefs[4].dflt}, {kTuneDefs[5].dflt}, {kTuneDefs[6].dflt}, {kTuneDefs[7].dflt},
-    {kTuneDefs[8].dflt}, {kTuneDefs[9].dflt}, {kTuneDefs[10].dflt}, {kTuneDefs[11].dflt}};
+    {kTuneDefs[8].dflt}, {kTuneDefs[9].dflt}, {kTuneDefs[10].dflt}};
 
 struct Knobs {
     uint32_t max_bn, pair_min_m;
     int pair;
-    uint32_t pair_single_tile, x_ring_bytes, max_x_stages, max_w_stages, grid, raster_gm, no_dp, no_pdl, co;
+    uint32_t pair_single_tile, x_ring_bytes, max_x_stages, max_w_stages, grid, raster_gm, no_dp, no_pdl;
 };
 Knobs knobs() {
     auto g = [](TuneId i) { return g_tune[i].load(std::memory_order_relaxed); };
@@ -409,7 +404,6 @@ Knobs knobs() {
     k.raster_gm = uint32_t(g(kTuneRasterGM));
     k.no_dp = uint32_t(g(kTuneNoDP));
     k.no_pdl = uint32_t(g(kTuneNoPDL));
-    k.co = uint32_t(g(kTuneCo));
     return k;
 }
 
@@ -466,35 +460,21 @@ int activation_tmap(const int8_t* d_x, uint32_t k, uint32_t m, int64_t ldx, uint
     return LQG_OK;
 }
 
-template <uint32_t kG, bool kFan, bool kPair, bool kCo = false>
-int set_smem_attr() {
-    static const cudaError_t e = [] {
-        auto fn = lqg_w4a8_gemm_kernel<kG, kFan, kPair, kCo>;
-        cudaError_t r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             kCo ? kSmemMaxCo : kSmemMax);
-        // the whole unified L1 as shared memory, so two co-resident CTAs fit
-        if (r == cudaSuccess)
-            r = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-        return r;
-    }();
-    if (e != cudaSuccess) return set_err(LQG_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
-    return LQG_OK;
-}
-
 // Co-resident 2-CTA clusters for the pair kernel at this shared-memory size
 // (not every SM can host half of a cluster: GPC / TPC boundaries), per device.
-int pair_clusters(int device, size_t smem, cudaLaunchConfig_t cfg) {
+int pair_clusters(int device, size_t smem, uint32_t grid) {
     static std::mutex mu;
     static std::vector<std::pair<std::pair<int, size_t>, int>> memo;
     std::lock_guard<std::mutex> lk(mu);
     for (auto& e : memo)
         if (e.first.first == device && e.first.second == smem) return e.second;
-    int nc = 0;
-    if (cudaOccupancyMaxActiveClusters(&nc, lqg_w4a8_gemm_kernel<1, false, true>, &cfg) != cudaSuccess) nc = 0;
-    cudaGetLastError();
+    const int nc = pair_clusters_kind3(smem, grid);
     memo.push_back({{device, smem}, nc});
     return nc;
 }
+
+// The kernels of each output kind live in their own translation unit.
+constexpr LaunchFn kLaunchByKind[4] = {launch_gemm_kind0, launch_gemm_kind1, launch_gemm_kind2, launch_gemm_kind3};
 
 // One launch over `ng` weight groups sharing n, k and group size (ng == 1: a
 // plain GEMM). Group e owns rows [row0_e, row0_e + m[e]) of X, token scales
@@ -549,14 +529,12 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
     const bool pair_legal = n_fan == 0 && (MT > 1 || K.pair_single_tile) && G.NT % 2 == 0 && w->num_sms >= 2;
     const bool pair = pair_legal && (K.pair == 1 || (K.pair == -1 && max_m >= K.pair_min_m));
     if (pair) BN = std::min(kMaxTileM, (BN + 31) / 32 * 32);
-    // Small token tiles run the co-resident kernel (half an SM per CTA), so
-    // consecutive GEMMs in a stream overlap their ramp and tail under PDL.
-    const bool co = !pair && n_fan == 0 && BN <= kSentinelMaxChunks * 16 && K.co;
     CUtensorMap tmap;
     {
         int rc = activation_tmap(d_x, G.k, m, ldx, pair ? BN / 2 : BN, &tmap);
         if (rc) return rc;
     }
+
 
     GroupTable<kMaxGroups> gt{};
     uint32_t tiles = 0, row0 = 0;
@@ -596,19 +574,20 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
     // activation tile issued behind d weight chunks lands only after them:
     // the X ring must run at least as far ahead as the W ring or the MMA
     // stalls on activations (measured: W 12 deep / X 8 deep at decode, W 8 /
-    // X 2 at M = 128). Both rings get the same depth (W even: the dequant
-    // warpgroups alternate), X takes any remaining space.
+    // X 2 at M = 128). Both rings get the same depth, X takes any remaining
+    // space.
     p.x_slot_bytes = (pair ? BN / 2 : BN) * kKBlock;
-    const uint32_t ring_budget = (co ? kSmemMaxCo : kSmemMax) - kSmemMisc;
+    const uint32_t ring_budget = kSmemMax - kSmemMisc;
     // Decode tiles (<= 32 tokens) keep the W ring at 6: deeper weight
     // prefetch only delays the activation tiles queued behind it (LLaMA-2-70B
     // 4-GEMM step at M = 16: 69 us at 6, 73 us at 10).
     const uint32_t w_cap = BN <= 32 ? kDecodeWStages : kMaxStages;
-    uint32_t sw = std::min({ring_budget / (p.x_slot_bytes + G.chunk_bytes), K.max_w_stages, w_cap}) & ~1u;
-    if (K.x_ring_bytes) sw = std::min(sw, std::max(2u, ((ring_budget - std::min(ring_budget, K.x_ring_bytes)) / G.chunk_bytes) & ~1u));
-    // even: the dequant warpgroups (which wait on the X tiles, see the
-    // kernel) alternate k-blocks
-    p.x_stages = std::min({(ring_budget - sw * G.chunk_bytes) / p.x_slot_bytes, K.max_x_stages, kMaxStages}) & ~1u;
+    // (ring sizes may be odd: each dequant warpgroup's ring position advances
+    // two slots per k-block with the parity of the slot's use count, see
+    // tmem_plan)
+    uint32_t sw = std::min({ring_budget / (p.x_slot_bytes + G.chunk_bytes), K.max_w_stages, w_cap});
+    if (K.x_ring_bytes) sw = std::min(sw, std::max(2u, (ring_budget - std::min(ring_budget, K.x_ring_bytes)) / G.chunk_bytes));
+    p.x_stages = std::min({(ring_budget - sw * G.chunk_bytes) / p.x_slot_bytes, K.max_x_stages, kMaxStages});
     if (p.x_stages < 2) return set_err(LQG_EVALIDATION, "tile configuration does not fit shared memory");
     p.w_base = p.x_stages * p.x_slot_bytes;
     // A split-K finisher of a large token tile gathers each contributor's
@@ -622,7 +601,7 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
     }
     if (sw < 2) return set_err(LQG_EVALIDATION, "tile configuration does not fit shared memory");
     p.w_stages = sw;
-    if (tmem_plan(BN, co ? kTmemColsCo : 512u).a_slots < 2)
+    if (tmem_plan(BN).a_slots < 2)
         return set_err(LQG_EVALIDATION, "tile configuration does not fit tensor memory");
     const uint64_t total_iters = uint64_t(tiles) * G.KB;
     if (total_iters * kMaxSlots >= (uint64_t(1) << 32))
@@ -636,37 +615,13 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
     const size_t smem = size_t(p.w_base) + size_t(p.w_stages) * G.chunk_bytes + kSmemMisc;
 
     DeviceGuard dg(w->device);
-    {
-        int rc = ng > 1 ? (pair ? set_smem_attr<kMaxGroups, false, true>()
-                                : co ? set_smem_attr<kMaxGroups, false, false, true>()
-                                     : set_smem_attr<kMaxGroups, false, false>())
-                        : (pair ? set_smem_attr<1, false, true>()
-                                : n_fan ? set_smem_attr<1, true, false>()
-                                        : co ? set_smem_attr<1, false, false, true>() : set_smem_attr<1, false, false>());
-        if (rc) return rc;
-    }
-    cudaLaunchConfig_t cfg{};
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[2];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = K.no_pdl ? 0 : 1;
-    attr[1].id = cudaLaunchAttributeClusterDimension;
-    attr[1].val.clusterDim.x = pair ? 2 : 1;
-    attr[1].val.clusterDim.y = 1;
-    attr[1].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = pair ? 2 : 1;
     if (pair) {
         // size the persistent grid to the clusters that are co-resident, so no
         // pair runs in a second wave
-        cfg.gridDim = dim3(2 * units);
-        const int nc = pair_clusters(w->device, smem, cfg);
+        const int nc = pair_clusters(w->device, smem, 2 * units);
         if (nc > 0 && uint32_t(nc) < units) units = uint32_t(nc);
         grid = 2 * units;
     }
-    cfg.gridDim = dim3(grid);
     // Hybrid schedule: whole-tile rounds first, stream-K over the last G..2G
     // tiles (all tiles when there are fewer than G), tiles rasterized in groups
     // of GM token tiles sized so that the activation and weight slices of one
@@ -684,26 +639,18 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
         if (K.raster_gm) gm = K.raster_gm;
         p.raster_gm = std::max(1u, std::min(gm, MT));
     }
-    if (ng > 1) {
-        if (pair)
-            LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<kMaxGroups, false, true>, tmap, p, gt));
-        else if (co)
-            LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<kMaxGroups, false, false, true>, tmap, p, gt));
-        else
-            LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<kMaxGroups, false, false>, tmap, p, gt));
-    } else {
-        GroupTable<1> g1{};
-        g1.e[0] = gt.e[0];
-        g1.n = 1;
-        if (pair)
-            LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<1, false, true>, tmap, p, g1));
-        else if (n_fan)
-            LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<1, true, false>, tmap, p, g1));
-        else if (co)
-            LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<1, false, false, true>, tmap, p, g1));
-        else
-            LQG_CUDA(cudaLaunchKernelEx(&cfg, lqg_w4a8_gemm_kernel<1, false, false>, tmap, p, g1));
-    }
+    KernelSpec ks;
+    ks.tmap_x = tmap;
+    ks.p = p;
+    ks.gt = &gt;
+    ks.ng = ng;
+    ks.pair = pair;
+    ks.fan = n_fan > 0;
+    ks.pdl = !K.no_pdl;
+    ks.grid = grid;
+    ks.smem = smem;
+    ks.stream = stream;
+    LQG_CUDA(kLaunchByKind[out_kind](ks));
     g_launches.fetch_add(1, std::memory_order_relaxed);
     LQG_CUDA(cudaGetLastError());
     return LQG_OK;

@@ -86,17 +86,14 @@ struct TmemPlan {
     uint32_t acc_stride, acc_stages, a_base, a_slots;
 };
 
-// TMEM columns per CTA: the whole SM (512), or half of it for the
-// co-resident decode kernel (kCo: two CTAs of consecutive launches share an SM).
-constexpr uint32_t kTmemColsCo = 256;
-
 // Double-buffered accumulators whenever two fit next to an A ring of >= 2
 // slots. Any ring size works with the two dequant warpgroups taking alternate
 // k-blocks: a warpgroup's ring position advances two slots per k-block and
 // flips its parity on every wrap, i.e. parity = (k-block / slots) & 1, the
 // parity of that slot's use count; a slot's next completion needs this
 // warpgroup's own write, so a wait can never be two phases behind.
-__host__ __device__ inline TmemPlan tmem_plan(uint32_t BN, uint32_t cols = 512) {
+__host__ __device__ inline TmemPlan tmem_plan(uint32_t BN) {
+    constexpr uint32_t cols = 512;
     TmemPlan t;
     t.acc_stride = (BN + 31) / 32 * 32;
     t.acc_stages = (2 * t.acc_stride + 2 * kACols <= cols) ? 2u : 1u;
@@ -133,6 +130,12 @@ struct GemmParams {
     uint32_t tiles;            // weight-tile x token-tile pairs (summed over groups)
     uint32_t sk_q, sk_r;       // stream-K iterations (tiles after the DP rounds x KB) = sk_q * units + sk_r
 };
+
+// Shared memory after the rings and barriers: TMEM address holder, then the
+// token scales of the current tile (double).
+constexpr uint32_t kMiscTsOff = 128;
+constexpr uint32_t kMiscBytes = kMiscTsOff + kMaxBN * 8;
+constexpr uint32_t kNumBarriers = 4 * kMaxStages + 2 * kMaxASlots + 5;
 
 // Grouped launch (MoE experts of one layer: same n, k, group size): the
 // tiles of every group form one linear space, tile-major within a group.
@@ -328,12 +331,8 @@ __device__ __forceinline__ void store_chunk_k(const GemmParams& p, uint32_t m0, 
         if (kKind == kOutAcc) {
             put(idx, acc[j]);
         } else {
-#ifdef LQG_EXP_FASTEPI  // timing experiment only: FP32 scaling (not bit-exact)
-            const float y = float(acc[j]) * float(cs_d) * float(ts[j]);
-#else
             const double a = i32_to_f64_exact(acc[j]);
             const float y = __double2float_rn(__dmul_rn(__dmul_rn(a, cs_d), ts[j]));
-#endif
             if (kKind == kOutF32)
                 put(idx, y);
             else if (kKind == kOutF16)
@@ -353,17 +352,6 @@ __device__ __forceinline__ void store_chunk_k(const GemmParams& p, uint32_t m0, 
 #pragma unroll
         for (uint32_t j = 0; j < 16; ++j)
             if (j < mend) one(j, idx0 + uint64_t(j) * uint64_t(p.ldo));
-    }
-}
-
-template <bool kFan>
-__device__ __forceinline__ void store_chunk(const GemmParams& p, uint32_t m0, uint32_t mlim, uint32_t n,
-                                            const int32_t (&acc)[16], double cs_d, const double* ts) {
-    switch (p.out_kind) {
-        case kOutAcc: store_chunk_k<kOutAcc, kFan>(p, m0, mlim, n, acc, cs_d, ts); break;
-        case kOutF32: store_chunk_k<kOutF32, kFan>(p, m0, mlim, n, acc, cs_d, ts); break;
-        case kOutF16: store_chunk_k<kOutF16, kFan>(p, m0, mlim, n, acc, cs_d, ts); break;
-        default: store_chunk_k<kOutBF16, kFan>(p, m0, mlim, n, acc, cs_d, ts); break;
     }
 }
 
@@ -403,16 +391,8 @@ struct UConst {
 // activation tile (N/2 tokens); the leader issues one M=256 MMA that reads the
 // B halves from both CTAs' shared memory, which halves the activation
 // shared-memory traffic per SM.
-// kCo: co-resident launch chain (small token tiles): half an SM per CTA
-// (<= 64 registers per thread, 256 TMEM columns, rings sized by the host to
-// half the shared memory), so under programmatic dependent launch the CTA of
-// the NEXT GEMM in the stream runs on the same SM as this one and streams and
-// dequantizes its first weight chunks (which do not depend on this GEMM)
-// while this one is still in its mainloop and split-K tail. The per-launch
-// ramp (prologue, first DRAM round trip) and tail then overlap instead of
-// adding up across consecutive GEMMs.
-template <uint32_t kG, bool kFan, bool kPair = false, bool kCo = false>
-__global__ void __launch_bounds__(kThreads, kCo ? 2 : 1)
+template <uint32_t kKind, uint32_t kG, bool kFan, bool kPair>
+__global__ void __launch_bounds__(kThreads, 1)
     lqg_w4a8_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const GemmParams p,
                          const __grid_constant__ GroupTable<kG> gt) {
     extern __shared__ uint8_t smem_raw[];
@@ -437,13 +417,13 @@ __global__ void __launch_bounds__(kThreads, kCo ? 2 : 1)
     const uint32_t fin_bar = bar_base + 8 * (kB + 2 * kMaxASlots + 4);  // split-K gather (finisher)
     uint8_t* misc = smem + ((ring_bytes + 7) & ~7u) + 8 * (kB + 2 * kMaxASlots + 5);
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(misc);
-    double* ts_s = reinterpret_cast<double*>(misc + 128);  // kMaxBN token scales, as double
+    double* ts_s = reinterpret_cast<double*>(misc + kMiscTsOff);  // kMaxBN token scales, as double
 
     const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const uint32_t G = sched_units(p);
     const uint32_t KB = p.KB;
-    constexpr uint32_t kTmemCols = kCo ? kTmemColsCo : 512u;
-    const TmemPlan tp = tmem_plan(p.BN, kTmemCols);
+    constexpr uint32_t kTmemCols = 512;
+    const TmemPlan tp = tmem_plan(p.BN);
     const uint32_t rank = kPair ? ptx::cluster_ctarank() : 0u;  // 0 = pair leader
     // barriers the pair leader waits on, as seen from this CTA
     auto leader = [&](uint32_t bar) { return kPair ? ptx::mapa(bar, 0) : bar; };
@@ -488,15 +468,11 @@ __global__ void __launch_bounds__(kThreads, kCo ? 2 : 1)
 #endif
     if (kPair) ptx::cluster_sync();  // the peer's barriers are initialised before any remote arrive
     ptx::tc_fence_after();
-    // A full-SM CTA owns all 512 TMEM columns, so its allocation starts at
-    // lane 0 / column 0 and TMEM addresses below are compile-time offsets;
-    // a co-resident CTA owns whichever half it was given.
-    uint32_t tmem_base = 0;
-    if constexpr (kCo) {
-        tmem_base = *tmem_holder;
-    } else {
-        if (*tmem_holder != 0) __trap();
-    }
+    // The CTA owns the SM's whole TMEM (512 columns, one CTA per SM), so the
+    // allocation always starts at lane 0 / column 0: TMEM addresses below are
+    // compile-time offsets (kept in uniform registers by the MMA warp).
+    if (*tmem_holder != 0) __trap();
+    constexpr uint32_t tmem_base = 0;
     // The schedule is recomputed by every thread from kernel parameters and
     // the block index (warp-uniform values, no shared-memory round trip).
     const Sched sch = make_sched(p);
@@ -731,38 +707,6 @@ __global__ void __launch_bounds__(kThreads, kCo ? 2 : 1)
                     sc = sa & 0xFFu;
                     a4 = (sa >> 8) * 0x01010101u;
                 };
-                if constexpr (kCo) {
-                    // Half-SM register budget: a quarter k-block at a time (two
-                    // sub-blocks = 16 words -> 16 TMEM columns), the W slot freed
-                    // once the last quarter's codes are consumed.
-#pragma unroll
-                    for (uint32_t qq = 0; qq < 4; ++qq) {
-                        uint4 v2[2];
-#pragma unroll
-                        for (uint32_t cc = 0; cc < 2; ++cc)
-                            v2[cc] = *reinterpret_cast<const uint4*>(wchunk + ((2 * qq + cc) * kTileN + row) * 16);
-                        if (qq == 0) {
-                            LQG_WAIT(dq_a, ptx::mbar_wait(aempty_bar(a.s), a.ph ^ 1));
-                            ptx::tc_fence_after();
-                        }
-                        int32_t o[16];
-#pragma unroll
-                        for (uint32_t cc = 0; cc < 2; ++cc) {
-                            uint32_t sc, a4;
-                            dq_param(2 * qq + cc, sc, a4);
-                            uint32_t* ou = reinterpret_cast<uint32_t*>(o) + 8 * cc;
-                            lqq_dequant_word(v2[cc].x, sc, a4, ou[0], ou[1]);
-                            lqq_dequant_word(v2[cc].y, sc, a4, ou[2], ou[3]);
-                            lqq_dequant_word(v2[cc].z, sc, a4, ou[4], ou[5]);
-                            lqq_dequant_word(v2[cc].w, sc, a4, ou[6], ou[7]);
-                        }
-                        if (qq == 3) {
-                            __syncwarp();
-                            if (lane == 0) ptx::mbar_arrive(wempty_bar(w.s));
-                        }
-                        ptx::tmem_st_x16(a_taddr + qq * 16, o);
-                    }
-                } else {
                 uint4 v[kSubBlocks];
 #ifdef LQG_EXP_NODQ  // timing experiment only: no code loads (garbage A)
 #pragma unroll
@@ -795,7 +739,6 @@ __global__ void __launch_bounds__(kThreads, kCo ? 2 : 1)
                 ptx::tc_fence_after();
                 ptx::tmem_st_x32(a_taddr, o[0]);
                 ptx::tmem_st_x32(a_taddr + 32, o[1]);
-                }  // !kCo
                 ptx::tmem_st_wait();
                 ptx::tc_fence_before();
                 wait_x();
@@ -830,7 +773,7 @@ __global__ void __launch_bounds__(kThreads, kCo ? 2 : 1)
         const uint32_t lane_addr = (sp * 32) << 16;
         const uint32_t et = threadIdx.x - kEpiWarp0 * 32;  // 0..127
         const uint32_t nchunks = p.BN / 16;
-        const bool scaled = p.out_kind != kOutAcc;
+        constexpr bool scaled = kKind != kOutAcc;
         ptx::griddep_wait();
         uint32_t as = 0, acc_ph = 0, fin_ph = 0;
         uint32_t i = 0;
@@ -867,12 +810,11 @@ __global__ void __launch_bounds__(kThreads, kCo ? 2 : 1)
             // segment's MMAs run; for small token tiles also request the first
             // batch's chunk-0 cells (they are usually published by now).
             const bool finisher = n_iters < KB && kb0 == 0;
-            // (the co-resident kernel only runs small token tiles)
-            const bool small = kCo || nchunks <= kSentinelMaxChunks;
+            const bool small = nchunks <= kSentinelMaxChunks;
             uint32_t c_first = 0, c_end = 0;
             // Split-K cells of up to kCB contributors for one 16-token chunk:
             // [contributor][quad]. Loaded one chunk ahead (software pipeline).
-            constexpr uint32_t kCB = kCo ? 1u : 4u;  // contributors per L2 round trip
+            constexpr uint32_t kCB = 4;  // contributors per L2 round trip
             int4 cb[kCB][4];
             auto cell_of = [&](uint32_t c, uint32_t ch) {
                 const uint32_t cs_slot = kPair ? 2 * c + rank : c;  // the matching CTA of a contributor pair
@@ -916,7 +858,7 @@ __global__ void __launch_bounds__(kThreads, kCo ? 2 : 1)
                         int32_t a[16];
 #pragma unroll
                         for (uint32_t j = 0; j < 16; ++j) a[j] = int32_t(v[j]);
-                        store_chunk<kFan>(p, m0 + ch * 16, mlim, n, a, cs, ts_s + ch * 16);
+                        store_chunk_k<kKind, kFan>(p, m0 + ch * 16, mlim, n, a, cs, ts_s + ch * 16);
                     }
                 }
             } else if (kb0 > 0) {
@@ -1006,7 +948,7 @@ __global__ void __launch_bounds__(kThreads, kCo ? 2 : 1)
                             }
                             if (c + kCB >= c_end && ch + 1 < nchunks) load_batch(c_first, ch + 1);
                         }
-                        if (n < p.N) store_chunk<kFan>(p, m0 + ch * 16, mlim, n, sum, cs, ts_s + ch * 16);
+                        if (n < p.N) store_chunk_k<kKind, kFan>(p, m0 + ch * 16, mlim, n, sum, cs, ts_s + ch * 16);
                     }
                 } else {
                     // Large token tiles: this is the CTA's last segment, so the
@@ -1059,11 +1001,7 @@ __global__ void __launch_bounds__(kThreads, kCo ? 2 : 1)
                                 const int4* scell = sm4 + b * (part_bytes / 16) + ch * 4 * kTileN + row;
 #pragma unroll
                                 for (uint32_t q = 0; q < 4; ++q) {
-#ifdef LQG_EXP_NOFINSUM  // timing experiment only: partials not read back
-                                    const int4 x = make_int4(q, b, ch, 0);
-#else
                                     const int4 x = scell[q * kTileN];
-#endif
                                     sum[4 * q] += x.x;
                                     sum[4 * q + 1] += x.y;
                                     sum[4 * q + 2] += x.z;
@@ -1075,12 +1013,7 @@ __global__ void __launch_bounds__(kThreads, kCo ? 2 : 1)
                                 ptx::tmem_st_x16(acc_taddr + ch * 16, sum);
                             } else {
                                 if (ch == 0 && et == 0) LQG_T(8);
-#ifdef LQG_EXP_NOFINSTORE  // timing experiment only: no final stores
-                                if (n < p.N && sum[0] == 0x7fffffff && sum[15] == 0x7ffffffe)
-#else
-                                if (n < p.N)
-#endif
-                                    store_chunk<kFan>(p, m0 + ch * 16, mlim, n, sum, cs, ts_s + ch * 16);
+                                if (n < p.N) store_chunk_k<kKind, kFan>(p, m0 + ch * 16, mlim, n, sum, cs, ts_s + ch * 16);
 #ifdef LQG_TRACE_PRO
                                 if (ch == 0 && et == 0) LQG_T(15);
 #endif
