@@ -355,6 +355,59 @@ __device__ __forceinline__ void store_chunk_k(const GemmParams& p, uint32_t m0, 
     }
 }
 
+// Final reduction of a split large-token tile: for chunks ch0, ch0+step, ...
+// the finisher's accumulator (TMEM) plus the nb gathered contributor
+// partials (shared memory, [contributor][chunk][quad][row] int4 cells), then
+// the scaled, cast output. Runs on the epilogue warps and, for the last batch,
+// on the idle dequant warps too (the team finish, see the dequant role).
+template <uint32_t kKind, bool kFan>
+__device__ __forceinline__ void finish_chunks(const GemmParams& p, uint32_t ch0, uint32_t step, uint32_t nchunks,
+                                              uint32_t acc_taddr, const int4* parts_smem, uint32_t nb,
+                                              uint32_t part_bytes, uint32_t row, uint32_t n, uint32_t m0,
+                                              uint32_t mlim, double cs, const double* ts_s) {
+    for (uint32_t ch = ch0; ch < nchunks; ch += step) {
+        uint32_t v[16];
+        ptx::tmem_ld_x16(acc_taddr + ch * 16, v);
+        ptx::tmem_ld_wait();
+        int32_t sum[16];
+#pragma unroll
+        for (uint32_t j = 0; j < 16; ++j) sum[j] = int32_t(v[j]);
+        for (uint32_t b = 0; b < nb; ++b) {
+            const int4* scell = parts_smem + b * (part_bytes / 16) + ch * 4 * kTileN + row;
+#pragma unroll
+            for (uint32_t q = 0; q < 4; ++q) {
+                const int4 x = scell[q * kTileN];
+                sum[4 * q] += x.x;
+                sum[4 * q + 1] += x.y;
+                sum[4 * q + 2] += x.z;
+                sum[4 * q + 3] += x.w;
+            }
+        }
+        if (n < p.N) store_chunk_k<kKind, kFan>(p, m0 + ch * 16, mlim, n, sum, cs, ts_s + ch * 16);
+    }
+}
+
+// Team work of the CTA's last segment (tiles of more than kSentinelMaxChunks
+// token chunks), from the schedule alone so that the dequant warps agree with
+// the epilogue warps: kTeamFinish = the head piece of a split tile (flag +
+// gather finisher). Measured and not done: a team publish of last-segment
+// contributor pieces (1-2 % slower) and team stores of a last whole tile
+// (neutral).
+enum TeamRole : uint32_t { kTeamNone = 0, kTeamFinish = 1, kTeamWhole = 2 };
+__device__ __forceinline__ uint32_t last_team_role(const GemmParams& p, uint32_t dp_rounds, uint32_t sk_beg,
+                                                   uint32_t sk_end) {
+    if (p.BN / 16 <= kSentinelMaxChunks) return kTeamNone;
+    if (sk_end == sk_beg) return dp_rounds ? kTeamWhole : kTeamNone;
+    const uint32_t last_tile = (sk_end - 1) / p.KB;  // relative to the stream-K tiles
+    const uint32_t seg_beg = max(sk_beg, last_tile * p.KB);
+    if (seg_beg > last_tile * p.KB) return kTeamNone;
+    return sk_end - seg_beg < p.KB ? kTeamFinish : kTeamWhole;
+}
+
+// Named barrier of the team finish: the 4 epilogue warps and 8 dequant warps.
+constexpr uint32_t kTeamBar = 2;
+constexpr uint32_t kTeamThreads = 12 * 32;
+
 #ifdef LQG_TRACE
 // Debug builds: per-CTA %globaltimer events and per-role wait cycles.
 __device__ unsigned long long g_lqg_trace[8 * 160 * 16];
@@ -418,6 +471,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* misc = smem + ((ring_bytes + 7) & ~7u) + 8 * (kB + 2 * kMaxASlots + 5);
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(misc);
     double* ts_s = reinterpret_cast<double*>(misc + kMiscTsOff);  // kMaxBN token scales, as double
+    uint32_t* team_info = reinterpret_cast<uint32_t*>(misc + 64);  // team finish: tile, acc column, nb
 
     const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const uint32_t G = sched_units(p);
@@ -766,6 +820,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             case 4: run(UConst<4>{}); break;
             default: run(UConst<8>{}); break;
         }
+        // Team finish (see the epilogue's large finisher): the last batch's
+        // reduction and stores of chunks 1 + wg, 4 + wg, ... of the
+        // finisher tile, once the epilogue warps have gathered it.
+        const uint32_t team = last_team_role(p, sch.dp_rounds, sch.sk_beg, sch.sk_end);
+        if (team == kTeamFinish) {
+            asm volatile("bar.sync %0, %1;" ::"n"(kTeamBar), "n"(kTeamThreads) : "memory");
+            ptx::tc_fence_after();
+            const TileRef tr = tile_ref(team_info[0], p, gt);
+            const uint32_t n = tr.nt * kTileN + row;
+            const double cs = kKind != kOutAcc ? double(tr.cs[n]) : 0.0;
+            const uint32_t acc_taddr = tmem_base + ((sp * 32) << 16) + team_info[1];
+            finish_chunks<kKind, kFan>(p, 1 + wg, 3, p.BN / 16, acc_taddr, reinterpret_cast<const int4*>(smem),
+                               team_info[2], p.BN * kTileN * 4, row, n, tr.row0, tr.mlim, cs, ts_s);
+            ptx::tc_fence_before();
+            asm volatile("bar.sync %0, %1;" ::"n"(kTeamBar), "n"(kTeamThreads) : "memory");
+        }
     } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
         // ------------------------------------------------------------ epilogue
         const uint32_t sp = warp % 4;
@@ -974,10 +1044,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef LQG_TRACE_PRO
                     if (et == 0) LQG_T(10);
 #endif
-                    for (uint32_t c0 = c_first; c0 < c_end; c0 += nb_max) {
+                    for (uint32_t c0 = c_first;; c0 += nb_max) {
                         const uint32_t nb = min(nb_max, c_end - c0);
                         const bool last_batch = c0 + nb >= c_end;
-                        if (et == 0) {
+                        if (et == 0 && nb) {
                             ptx::fence_proxy_async();  // acquired data + prior generic SMEM reads vs TMA
                             ptx::mbar_arrive_expect_tx(fin_bar, nb * part_bytes);
                             for (uint32_t b = 0; b < nb; ++b)
@@ -985,42 +1055,59 @@ __global__ void __launch_bounds__(kThreads, 1)
                                               p.parts + uint64_t(kPair ? 2 * (c0 + b) + rank : c0 + b) * kSlotCellsK + kSmallCells,
                                               part_bytes, fin_bar, ptx::policy_evict_first());
                         }
-                        ptx::mbar_wait(fin_bar, fin_ph);
-                        fin_ph ^= 1;
+                        if (nb) {
+                            ptx::mbar_wait(fin_bar, fin_ph);
+                            fin_ph ^= 1;
+                        }
 #ifdef LQG_TRACE_PRO
                         if (et == 0) LQG_T(11);
 #endif
-                        for (uint32_t ch = 0; ch < nchunks; ++ch) {
-                            uint32_t v[16];
-                            ptx::tmem_ld_x16(acc_taddr + ch * 16, v);
-                            ptx::tmem_ld_wait();
-                            int32_t sum[16];
+                        if (!last_batch) {
+                            // running sum back into the accumulator for the next batch
+                            for (uint32_t ch = 0; ch < nchunks; ++ch) {
+                                uint32_t v[16];
+                                ptx::tmem_ld_x16(acc_taddr + ch * 16, v);
+                                ptx::tmem_ld_wait();
+                                int32_t sum[16];
 #pragma unroll
-                            for (uint32_t j = 0; j < 16; ++j) sum[j] = int32_t(v[j]);
-                            for (uint32_t b = 0; b < nb; ++b) {
-                                const int4* scell = sm4 + b * (part_bytes / 16) + ch * 4 * kTileN + row;
+                                for (uint32_t j = 0; j < 16; ++j) sum[j] = int32_t(v[j]);
+                                for (uint32_t b = 0; b < nb; ++b) {
+                                    const int4* scell = sm4 + b * (part_bytes / 16) + ch * 4 * kTileN + row;
 #pragma unroll
-                                for (uint32_t q = 0; q < 4; ++q) {
-                                    const int4 x = scell[q * kTileN];
-                                    sum[4 * q] += x.x;
-                                    sum[4 * q + 1] += x.y;
-                                    sum[4 * q + 2] += x.z;
-                                    sum[4 * q + 3] += x.w;
+                                    for (uint32_t q = 0; q < 4; ++q) {
+                                        const int4 x = scell[q * kTileN];
+                                        sum[4 * q] += x.x;
+                                        sum[4 * q + 1] += x.y;
+                                        sum[4 * q + 2] += x.z;
+                                        sum[4 * q + 3] += x.w;
+                                    }
                                 }
-                            }
-                            if (!last_batch) {
-                                // running sum back into the accumulator for the next batch
                                 ptx::tmem_st_x16(acc_taddr + ch * 16, sum);
-                            } else {
-                                if (ch == 0 && et == 0) LQG_T(8);
-                                if (n < p.N) store_chunk_k<kKind, kFan>(p, m0 + ch * 16, mlim, n, sum, cs, ts_s + ch * 16);
-#ifdef LQG_TRACE_PRO
-                                if (ch == 0 && et == 0) LQG_T(15);
-#endif
                             }
+                            ptx::tmem_st_wait();
+                            asm volatile("bar.sync 1, 128;" ::: "memory");  // ring reads done before the next batch
+                        } else {
+                            // Last batch: the team finish. This is the CTA's last
+                            // segment, so the 8 dequant warps are idle: they take
+                            // two of every three chunks (each warp reads its own
+                            // TMEM sub-partition, warp % 4), which cuts the
+                            // serial tail of the launch.
+                            if (et == 0) {
+                                team_info[0] = tile;
+                                team_info[1] = acc_taddr & 0xFFFFu;
+                                team_info[2] = nb;
+                            }
+                            ptx::tc_fence_before();
+                            asm volatile("bar.sync %0, %1;" ::"n"(kTeamBar), "n"(kTeamThreads) : "memory");
+                            ptx::tc_fence_after();
+                            if (et == 0) LQG_T(8);
+                            finish_chunks<kKind, kFan>(p, 0, 3, nchunks, acc_taddr, sm4, nb, part_bytes, row, n, m0,
+                                                       mlim, cs, ts_s);
+                            ptx::tc_fence_before();
+                            asm volatile("bar.sync %0, %1;" ::"n"(kTeamBar), "n"(kTeamThreads) : "memory");
+                            ptx::tc_fence_after();
+                            break;
                         }
-                        if (!last_batch) ptx::tmem_st_wait();
-                        asm volatile("bar.sync 1, 128;" ::: "memory");  // ring reads done before the next batch
                     }
 #ifdef LQG_TRACE_PRO
                     if (et == 0) LQG_T(14);
