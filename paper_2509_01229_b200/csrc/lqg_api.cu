@@ -692,10 +692,17 @@ const char* lqg_last_error(void) { return g_err.c_str(); }
 #ifdef LQG_TRACE
 // Debug build only: copy the per-CTA %globaltimer trace (160 x 16 u64).
 int lqg_debug_trace(unsigned long long* out) {
-    return cudaMemcpyFromSymbol(out, g_lqg_trace, sizeof(unsigned long long) * 8 * 160 * 16) ==
-                   cudaSuccess
-               ? 0
-               : 4;
+    // each kernel unit (output kind) has its own trace buffer: merge them
+    constexpr size_t kN = 8 * 160 * 16;
+    std::vector<unsigned long long> buf(kN);
+    std::fill(out, out + kN, 0ull);
+    int (*const fns[4])(unsigned long long*) = {debug_trace_kind0, debug_trace_kind1, debug_trace_kind2,
+                                                debug_trace_kind3};
+    for (auto fn : fns) {
+        if (fn(buf.data())) return 4;
+        for (size_t i = 0; i < kN; ++i) out[i] = std::max(out[i], buf[i]);
+    }
+    return 0;
 }
 #endif
 const char* lqg_version(void) { return "lqg 0.1 (sm_100a, tcgen05 kind::i8, TMEM-A LiquidQuant mainloop)"; }

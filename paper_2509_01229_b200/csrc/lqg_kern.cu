@@ -71,4 +71,14 @@ int LQG_CAT(pair_clusters_kind, LQG_KIND)(size_t smem, uint32_t grid) {
     return nc;
 }
 
+// LQG_TRACE builds: this unit's per-CTA event buffer (zeros otherwise).
+int LQG_CAT(debug_trace_kind, LQG_KIND)(unsigned long long* out) {
+#ifdef LQG_TRACE
+    return cudaMemcpyFromSymbol(out, g_lqg_trace, sizeof(unsigned long long) * 8 * 160 * 16) == cudaSuccess ? 0 : 4;
+#else
+    for (size_t i = 0; i < size_t(8) * 160 * 16; ++i) out[i] = 0;
+    return 0;
+#endif
+}
+
 }  // namespace lqg

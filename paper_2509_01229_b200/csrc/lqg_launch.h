@@ -30,7 +30,8 @@ using PairClustersFn = int (*)(size_t smem, uint32_t grid);
 
 #define LQG_DECLARE_KIND(K)                               \
     cudaError_t launch_gemm_kind##K(const KernelSpec& k); \
-    int pair_clusters_kind##K(size_t smem, uint32_t grid);
+    int pair_clusters_kind##K(size_t smem, uint32_t grid); \
+    int debug_trace_kind##K(unsigned long long* out);
 LQG_DECLARE_KIND(0)
 LQG_DECLARE_KIND(1)
 LQG_DECLARE_KIND(2)

@@ -56,8 +56,9 @@ print(f"{sys.argv[1]} {' '.join(sys.argv[2:])}: {copies} launches in {e0.elapsed
 buf = np.zeros(8 * 160 * 16, np.uint64)
 _lib.lib().lqg_debug_trace(buf.ctypes.data_as(ctypes.c_void_p))
 allr = buf.reshape(8, 160, 16).astype(np.int64)
-order = sorted(range(8), key=lambda sl: allr[sl][allr[sl][:, 0] > 0, 0].min())
-t0 = min(allr[sl][allr[sl][:, 0] > 0, 0].min() for sl in range(8))
+live = [sl for sl in range(8) if (allr[sl][:, 0] > 0).any()]
+order = sorted(live, key=lambda sl: allr[sl][allr[sl][:, 0] > 0, 0].min())
+t0 = min(allr[sl][allr[sl][:, 0] > 0, 0].min() for sl in live)
 print("  launch:   entry[min,max]   PDL-rel   MMA[first,last]  acc[med,max] pub-max  epi-done[med,max]  exit[min,max]  (us)")
 for sl in order:
     r = allr[sl]
