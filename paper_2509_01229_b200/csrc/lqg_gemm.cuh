@@ -135,7 +135,7 @@ struct GemmParams {
 // token scales of the current tile (double).
 constexpr uint32_t kMiscTsOff = 128;
 constexpr uint32_t kMiscBytes = kMiscTsOff + kMaxBN * 8;
-constexpr uint32_t kNumBarriers = 4 * kMaxStages + 2 * kMaxASlots + 5;
+constexpr uint32_t kNumBarriers = 4 * kMaxStages + 2 * kMaxASlots + 7;
 
 // Grouped launch (MoE experts of one layer: same n, k, group size): the
 // tiles of every group form one linear space, tile-major within a group.
@@ -404,9 +404,13 @@ __device__ __forceinline__ uint32_t last_team_role(const GemmParams& p, uint32_t
     return sk_end - seg_beg < p.KB ? kTeamFinish : kTeamWhole;
 }
 
-// Named barrier of the team finish: the 4 epilogue warps and 8 dequant warps.
-constexpr uint32_t kTeamBar = 2;
-constexpr uint32_t kTeamThreads = 12 * 32;
+// Named barrier 1 of the 4 epilogue warps (bar.sync is warp-aligned: the warp
+// reconverges first, as the mbarrier try_wait loops before it are invisible
+// to the compiler's reconvergence analysis).
+__device__ __forceinline__ void epi_bar() {
+    __syncwarp();
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+}
 
 #ifdef LQG_TRACE
 // Debug builds: per-CTA %globaltimer events and per-role wait cycles.
@@ -468,7 +472,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto accfull_bar = [&](uint32_t a) { return bar_base + 8 * (kB + 2 * kMaxASlots + a); };
     auto accempty_bar = [&](uint32_t a) { return bar_base + 8 * (kB + 2 * kMaxASlots + 2 + a); };
     const uint32_t fin_bar = bar_base + 8 * (kB + 2 * kMaxASlots + 4);  // split-K gather (finisher)
-    uint8_t* misc = smem + ((ring_bytes + 7) & ~7u) + 8 * (kB + 2 * kMaxASlots + 5);
+    // team finish hand-over: epilogue -> dequant warps (tile gathered), and back
+    const uint32_t team_ready = bar_base + 8 * (kB + 2 * kMaxASlots + 5);
+    const uint32_t team_done = bar_base + 8 * (kB + 2 * kMaxASlots + 6);
+    uint8_t* misc = smem + ((ring_bytes + 7) & ~7u) + 8 * (kB + 2 * kMaxASlots + 7);
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(misc);
     double* ts_s = reinterpret_cast<double*>(misc + kMiscTsOff);  // kMaxBN token scales, as double
     uint32_t* team_info = reinterpret_cast<uint32_t*>(misc + 64);  // team finish: tile, acc column, nb
@@ -501,7 +508,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_init(accfull_bar(lane), 1);
             ptx::mbar_init(accempty_bar(lane), kPair ? 8 : 4);  // one arrive per epilogue warp
         }
-        if (lane == 0) ptx::mbar_init(fin_bar, 1);
+        if (lane == 0) {
+            ptx::mbar_init(fin_bar, 1);
+            ptx::mbar_init(team_ready, 1);         // the epilogue's leading thread
+            ptx::mbar_init(team_done, kDQWarps);   // one arrive per dequant warp
+        }
         ptx::fence_mbar_init();
     }
     if (warp == kWarpX && lane == 0) ptx::prefetch_tmap(&tmap_x);
@@ -825,7 +836,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // finisher tile, once the epilogue warps have gathered it.
         const uint32_t team = last_team_role(p, sch.dp_rounds, sch.sk_beg, sch.sk_end);
         if (team == kTeamFinish) {
-            asm volatile("bar.sync %0, %1;" ::"n"(kTeamBar), "n"(kTeamThreads) : "memory");
+            ptx::mbar_wait(team_ready, 0);
             ptx::tc_fence_after();
             const TileRef tr = tile_ref(team_info[0], p, gt);
             const uint32_t n = tr.nt * kTileN + row;
@@ -834,7 +845,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             finish_chunks<kKind, kFan>(p, 1 + wg, 3, p.BN / 16, acc_taddr, reinterpret_cast<const int4*>(smem),
                                team_info[2], p.BN * kTileN * 4, row, n, tr.row0, tr.mlim, cs, ts_s);
             ptx::tc_fence_before();
-            asm volatile("bar.sync %0, %1;" ::"n"(kTeamBar), "n"(kTeamThreads) : "memory");
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(team_done);
         }
     } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
         // ------------------------------------------------------------ epilogue
@@ -903,7 +915,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 split_contributors(tile - sch.sk_tile0, KB, G, p.sk_q, p.sk_r, c_first, c_end);
                 if (small) load_batch(c_first, 0);
             }
-            asm volatile("bar.sync 1, 128;" ::: "memory");
+            epi_bar();
 #ifdef LQG_EXP_SPINACC
             ptx::mbar_wait(accfull_bar(as), acc_ph);
 #else
@@ -956,7 +968,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (!small) {
                     // large tiles: every epilogue thread's stores, then one release flag
                     __threadfence();
-                    asm volatile("bar.sync 1, 128;" ::: "memory");
+                    epi_bar();
                     if (et == 0) ptx::st_release_u32(p.flags + blockIdx.x, 1u);
                 }
                 if (et == 0) LQG_T(7);
@@ -1040,7 +1052,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         while (ptx::ld_acquire_u32(p.flags + fc) == 0) __nanosleep(32);
                         p.flags[fc] = 0;
                     }
-                    asm volatile("bar.sync 1, 128;" ::: "memory");
+                    epi_bar();
 #ifdef LQG_TRACE_PRO
                     if (et == 0) LQG_T(10);
 #endif
@@ -1085,26 +1097,25 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 ptx::tmem_st_x16(acc_taddr + ch * 16, sum);
                             }
                             ptx::tmem_st_wait();
-                            asm volatile("bar.sync 1, 128;" ::: "memory");  // ring reads done before the next batch
+                            epi_bar();  // ring reads done before the next batch
                         } else {
                             // Last batch: the team finish. This is the CTA's last
                             // segment, so the 8 dequant warps are idle: they take
                             // two of every three chunks (each warp reads its own
                             // TMEM sub-partition, warp % 4), which cuts the
                             // serial tail of the launch.
+                            epi_bar();  // token scales, gathered partials seen by et 0
                             if (et == 0) {
                                 team_info[0] = tile;
                                 team_info[1] = acc_taddr & 0xFFFFu;
                                 team_info[2] = nb;
+                                ptx::tc_fence_before();
+                                ptx::mbar_arrive(team_ready);  // release: team_info, ts_s, SMEM partials
+                                LQG_T(8);
                             }
-                            ptx::tc_fence_before();
-                            asm volatile("bar.sync %0, %1;" ::"n"(kTeamBar), "n"(kTeamThreads) : "memory");
-                            ptx::tc_fence_after();
-                            if (et == 0) LQG_T(8);
                             finish_chunks<kKind, kFan>(p, 0, 3, nchunks, acc_taddr, sm4, nb, part_bytes, row, n, m0,
                                                        mlim, cs, ts_s);
-                            ptx::tc_fence_before();
-                            asm volatile("bar.sync %0, %1;" ::"n"(kTeamBar), "n"(kTeamThreads) : "memory");
+                            ptx::mbar_wait(team_done, 0);  // the dequant warps' chunks are read
                             ptx::tc_fence_after();
                             break;
                         }
@@ -1115,7 +1126,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 release_acc(cur_as);
             }
-            asm volatile("bar.sync 1, 128;" ::: "memory");  // ts_s reuse
+            epi_bar();  // ts_s reuse
         }
 #ifdef LQG_TRACE_PRO
         if (et == 0) LQG_T(13);
@@ -1123,6 +1134,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 
     ptx::tc_fence_before();
+    __syncwarp();  // reconverge after the roles' try_wait loops (aligned barrier)
     __syncthreads();
 #ifdef LQG_TRACE_PRO
     if (threadIdx.x == 0) LQG_T(12);
