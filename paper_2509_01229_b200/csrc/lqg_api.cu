@@ -361,7 +361,7 @@ constexpr uint32_t kSmemMisc = (1024 + 8 * kNumBarriers + 8 + kMiscBytes + 1023)
 // tests change them through lqg_tune_set (process-wide, no environment reads).
 enum TuneId : int {
     kTuneMaxBN, kTunePairMinM, kTunePair, kTunePairSingleTile, kTuneXRingBytes, kTuneMaxXStages,
-    kTuneMaxWStages, kTuneGrid, kTuneRasterGM, kTuneNoDP, kTuneNoPDL, kTuneCount
+    kTuneMaxWStages, kTuneGrid, kTuneRasterGM, kTuneNoDP, kTuneNoPDL, kTuneAccStages, kTuneCount
 };
 struct TuneDef {
     const char* name;
@@ -379,16 +379,17 @@ constexpr TuneDef kTuneDefs[kTuneCount] = {
     {"raster_gm", 0, 0, 1 << 20},                  // 0 = derived
     {"no_dp", 0, 0, 1},                            // stream-K over all tiles
     {"no_pdl", 0, 0, 1},                           // no programmatic dependent launch
+    {"acc_stages", 2, 1, 2},                       // accumulator stages in TMEM (the rest is A ring)
 };
 std::atomic<int64_t> g_tune[kTuneCount] = {
     {kTuneDefs[0].dflt}, {kTuneDefs[1].dflt}, {kTuneDefs[2].dflt}, {kTuneDefs[3].dflt},
     {kTuneDefs[4].dflt}, {kTuneDefs[5].dflt}, {kTuneDefs[6].dflt}, {kTuneDefs[7].dflt},
-    {kTuneDefs[8].dflt}, {kTuneDefs[9].dflt}, {kTuneDefs[10].dflt}};
+    {kTuneDefs[8].dflt}, {kTuneDefs[9].dflt}, {kTuneDefs[10].dflt}, {kTuneDefs[11].dflt}};
 
 struct Knobs {
     uint32_t max_bn, pair_min_m;
     int pair;
-    uint32_t pair_single_tile, x_ring_bytes, max_x_stages, max_w_stages, grid, raster_gm, no_dp, no_pdl;
+    uint32_t pair_single_tile, x_ring_bytes, max_x_stages, max_w_stages, grid, raster_gm, no_dp, no_pdl, acc_stages;
 };
 Knobs knobs() {
     auto g = [](TuneId i) { return g_tune[i].load(std::memory_order_relaxed); };
@@ -404,6 +405,7 @@ Knobs knobs() {
     k.raster_gm = uint32_t(g(kTuneRasterGM));
     k.no_dp = uint32_t(g(kTuneNoDP));
     k.no_pdl = uint32_t(g(kTuneNoPDL));
+    k.acc_stages = uint32_t(g(kTuneAccStages));
     return k;
 }
 
@@ -601,7 +603,8 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
     }
     if (sw < 2) return set_err(LQG_EVALIDATION, "tile configuration does not fit shared memory");
     p.w_stages = sw;
-    if (tmem_plan(BN).a_slots < 2)
+    p.acc_stages = K.acc_stages;
+    if (tmem_plan(BN, p.acc_stages).a_slots < 2)
         return set_err(LQG_EVALIDATION, "tile configuration does not fit tensor memory");
     const uint64_t total_iters = uint64_t(tiles) * G.KB;
     if (total_iters * kMaxSlots >= (uint64_t(1) << 32))

@@ -92,11 +92,11 @@ struct TmemPlan {
 // flips its parity on every wrap, i.e. parity = (k-block / slots) & 1, the
 // parity of that slot's use count; a slot's next completion needs this
 // warpgroup's own write, so a wait can never be two phases behind.
-__host__ __device__ inline TmemPlan tmem_plan(uint32_t BN) {
+__host__ __device__ inline TmemPlan tmem_plan(uint32_t BN, uint32_t max_acc_stages = 2) {
     constexpr uint32_t cols = 512;
     TmemPlan t;
     t.acc_stride = (BN + 31) / 32 * 32;
-    t.acc_stages = (2 * t.acc_stride + 2 * kACols <= cols) ? 2u : 1u;
+    t.acc_stages = (max_acc_stages >= 2 && 2 * t.acc_stride + 2 * kACols <= cols) ? 2u : 1u;
     t.a_base = (t.acc_stages * t.acc_stride + kACols - 1) / kACols * kACols;
     t.a_slots = (cols - t.a_base) / kACols;
     if (t.a_slots > kMaxASlots) t.a_slots = kMaxASlots;
@@ -129,6 +129,7 @@ struct GemmParams {
                                //    and loads half of every activation tile
     uint32_t tiles;            // weight-tile x token-tile pairs (summed over groups)
     uint32_t sk_q, sk_r;       // stream-K iterations (tiles after the DP rounds x KB) = sk_q * units + sk_r
+    uint32_t acc_stages;       // at most this many accumulator stages in TMEM (1 or 2; see tmem_plan)
 };
 
 // Shared memory after the rings and barriers: TMEM address holder, then the
@@ -484,7 +485,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t G = sched_units(p);
     const uint32_t KB = p.KB;
     constexpr uint32_t kTmemCols = 512;
-    const TmemPlan tp = tmem_plan(p.BN);
+    const TmemPlan tp = tmem_plan(p.BN, p.acc_stages);
     const uint32_t rank = kPair ? ptx::cluster_ctarank() : 0u;  // 0 = pair leader
     // barriers the pair leader waits on, as seen from this CTA
     auto leader = [&](uint32_t bar) { return kPair ? ptx::mapa(bar, 0) : bar; };

@@ -618,7 +618,8 @@ def test_pair_threshold_boundary_is_seamless(torch_cuda, lqg):
                                    (200, 256, 8192), (700, 512, 1536)])
 @pytest.mark.parametrize("knobs", [dict(max_w_stages=2), dict(max_w_stages=4, x_ring_bytes=1024),
                                    dict(max_x_stages=2, x_ring_bytes=1024), dict(grid=7), dict(grid=64, no_dp=1),
-                                   dict(max_bn=32), dict(pair=1, pair_single_tile=1), dict(no_pdl=1)])
+                                   dict(max_bn=32), dict(pair=1, pair_single_tile=1), dict(no_pdl=1),
+                                   dict(acc_stages=1)])
 def test_schedule_knobs_bit_exact(torch_cuda, lqg, m, n, k, knobs):
     """Every ring split (2-stage W ring, minimal X ring), grid size, token
     tile and pair policy gives the same INT32 accumulators and BF16 outputs as
