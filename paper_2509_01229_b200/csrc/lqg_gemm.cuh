@@ -136,7 +136,7 @@ struct GemmParams {
 // token scales of the current tile (double).
 constexpr uint32_t kMiscTsOff = 128;
 constexpr uint32_t kMiscBytes = kMiscTsOff + kMaxBN * 8;
-constexpr uint32_t kNumBarriers = 4 * kMaxStages + 2 * kMaxASlots + 7;
+constexpr uint32_t kNumBarriers = 4 * kMaxStages + 3 * kMaxASlots + 7;
 
 // Grouped launch (MoE experts of one layer: same n, k, group size): the
 // tiles of every group form one linear space, tile-major within a group.
@@ -413,6 +413,19 @@ __device__ __forceinline__ void epi_bar() {
     asm volatile("bar.sync 1, 128;" ::: "memory");
 }
 
+#ifdef LQG_TRACE_KB
+// Debug builds: per-k-block clock64 events of CTA 0 (k-blocks 0..63):
+// 0 W issued, 1 X issued, 2 dequant W ready, 3 dequant A slot free,
+// 4 dequant A published, 5 MMA A ready, 6 MMA issued.
+__device__ long long g_lqg_kb[64 * 8];
+#define LQG_KB(i, e)                                                              \
+    do {                                                                          \
+        if (blockIdx.x == 0 && (i) < 64) g_lqg_kb[(i) * 8 + (e)] = clock64();     \
+    } while (0)
+#else
+#define LQG_KB(i, e) ((void)0)
+#endif
+
 #ifdef LQG_TRACE
 // Debug builds: per-CTA %globaltimer events and per-role wait cycles.
 __device__ unsigned long long g_lqg_trace[8 * 160 * 16];
@@ -476,7 +489,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     // team finish hand-over: epilogue -> dequant warps (tile gathered), and back
     const uint32_t team_ready = bar_base + 8 * (kB + 2 * kMaxASlots + 5);
     const uint32_t team_done = bar_base + 8 * (kB + 2 * kMaxASlots + 6);
-    uint8_t* misc = smem + ((ring_bytes + 7) & ~7u) + 8 * (kB + 2 * kMaxASlots + 7);
+    // first half of an A slot (K columns 0..127) read: the MMA warp commits after
+    // the k-block's first four MMAs
+    auto aempty_lo_bar = [&](uint32_t a) { return bar_base + 8 * (kB + 2 * kMaxASlots + 7 + a); };
+    uint8_t* misc = smem + ((ring_bytes + 7) & ~7u) + 8 * (kB + 3 * kMaxASlots + 7);
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(misc);
     double* ts_s = reinterpret_cast<double*>(misc + kMiscTsOff);  // kMaxBN token scales, as double
     uint32_t* team_info = reinterpret_cast<uint32_t*>(misc + 64);  // team finish: tile, acc column, nb
@@ -504,6 +520,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane < kMaxASlots) {
             ptx::mbar_init(afull_bar(lane), kPair ? 8 : 4);  // the dequant WG's warps (of both CTAs)
             ptx::mbar_init(aempty_bar(lane), 1);
+            ptx::mbar_init(aempty_lo_bar(lane), 1);
         }
         if (lane < 2) {
             ptx::mbar_init(accfull_bar(lane), 1);
@@ -575,6 +592,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (ptx::elect_one()) {
                 ptx::mbar_arrive_expect_tx(wfull_bar(w.s), p.chunk_bytes);
                 ptx::bulk_g2s(smem_base + p.w_base + w.s * p.chunk_bytes, src, p.chunk_bytes, wfull_bar(w.s), pol_w);
+                LQG_KB(i, 0);
             }
             __syncwarp();
             if (ww.next(p))
@@ -616,6 +634,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::tma_2d_g2s(slot, &tmap_x, k0, m0, xfull_bar(x.s), pol_x);
                     ptx::tma_2d_g2s(slot + atom_bytes, &tmap_x, k0 + int32_t(kXAtom), m0, xfull_bar(x.s), pol_x);
                 }
+                LQG_KB(i, 1);
             }
             __syncwarp();
             if (xw.next(p)) xrow0 = tile_ref(xw.tile, p, gt).row0;
@@ -665,6 +684,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         for (uint32_t i = 0; i < n_local; ++i) {
             wait_ready();
+            if (lane == 0) LQG_KB(i, 5);
             if (i == 0 && lane == 0) LQG_T(4);
             if (i + 1 == n_local && lane == 0) LQG_T(5);
             const bool seg_end = seg_left == 1;
@@ -675,11 +695,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t d_tmem = tmem_base + as * tp.acc_stride;
                 const uint32_t a_tmem = tmem_base + tp.a_base + a.s * kACols;
                 const uint64_t bdesc = desc0 + uint64_t(x.s * slot_desc);
+                // The first half of the A slot is free once the first four
+                // MMAs have read it: its own commit lets the dequant warps
+                // refill that half while the second half is still being read.
 #pragma unroll
-                for (uint32_t k8 = 0; k8 < kSubBlocks; ++k8) mma(d_tmem, a_tmem, bdesc, k8, seg_start && k8 == 0);
+                for (uint32_t k8 = 0; k8 < kSubBlocks / 2; ++k8) mma(d_tmem, a_tmem, bdesc, k8, seg_start && k8 == 0);
+                commit(aempty_lo_bar(a.s));
+#pragma unroll
+                for (uint32_t k8 = kSubBlocks / 2; k8 < kSubBlocks; ++k8) mma(d_tmem, a_tmem, bdesc, k8, false);
                 commit(xempty_bar(x.s));
                 commit(aempty_bar(a.s));
                 if (seg_end) commit(accfull_bar(as));
+                LQG_KB(i, 6);
             }
             __syncwarp();
 #ifdef LQG_TRACE
@@ -747,6 +774,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 continue;
 #endif
                 LQG_WAIT(dq_w, ptx::mbar_wait(wfull_bar(w.s), w.ph));
+                if (warp % 4 == 2 && lane == 0) LQG_KB(i, 2);
                 const uint8_t* wchunk = wring + w.s * p.chunk_bytes;
                 // all P group parameters of this row: one 2..16-byte LDS
                 uint32_t prm[(P + 1) / 2];
@@ -801,11 +829,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // every code of the chunk has been consumed: free the W slot
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(wempty_bar(w.s));
-                LQG_WAIT(dq_a, ptx::mbar_wait(aempty_bar(a.s), a.ph ^ 1));
+                // Half by half: the first half of the slot is rewritten as soon
+                // as the previous k-block's first four MMAs have read it.
+                LQG_WAIT(dq_a, ptx::mbar_wait(aempty_lo_bar(a.s), a.ph ^ 1));
+                if (warp % 4 == 2 && lane == 0) LQG_KB(i, 3);
                 ptx::tc_fence_after();
                 ptx::tmem_st_x32(a_taddr, o[0]);
+                ptx::mbar_wait(aempty_bar(a.s), a.ph ^ 1);
+                ptx::tc_fence_after();
                 ptx::tmem_st_x32(a_taddr + 32, o[1]);
                 ptx::tmem_st_wait();
+                if (warp % 4 == 2 && lane == 0) LQG_KB(i, 7);
                 ptx::tc_fence_before();
                 wait_x();
                 __syncwarp();
@@ -814,6 +848,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         ptx::mbar_arrive_cluster_relaxed(leader(afull_bar(a.s)));
                     else
                         ptx::mbar_arrive(afull_bar(a.s));
+                    if (warp % 4 == 2) LQG_KB(i, 4);
                 }
                 w.adv(2, SW);
                 a.adv(2, tp.a_slots);
