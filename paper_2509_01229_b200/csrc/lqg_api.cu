@@ -584,12 +584,16 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
     // prefetch only delays the activation tiles queued behind it (LLaMA-2-70B
     // 4-GEMM step at M = 16: 69 us at 6, 73 us at 10).
     const uint32_t w_cap = BN <= 32 ? kDecodeWStages : kMaxStages;
-    // (ring sizes may be odd: each dequant warpgroup's ring position advances
-    // two slots per k-block with the parity of the slot's use count, see
-    // tmem_plan)
-    uint32_t sw = std::min({ring_budget / (p.x_slot_bytes + G.chunk_bytes), K.max_w_stages, w_cap});
-    if (K.x_ring_bytes) sw = std::min(sw, std::max(2u, (ring_budget - std::min(ring_budget, K.x_ring_bytes)) / G.chunk_bytes));
-    p.x_stages = std::min({(ring_budget - sw * G.chunk_bytes) / p.x_slot_bytes, K.max_x_stages, kMaxStages});
+    // Both rings are EVEN: the two dequant warpgroups take alternate
+    // k-blocks and wait on the W (and X) full barriers by parity; with an even
+    // ring each warpgroup owns its slots, so the phase before the one it waits
+    // for is its own, already consumed. With an odd ring that phase belongs to
+    // the other warpgroup, whose TMA may still be in flight: a warpgroup
+    // running ahead then sees the parity of the phase two back and reads a
+    // slot that has not landed (found by tools/pair_stress.py).
+    uint32_t sw = std::min({ring_budget / (p.x_slot_bytes + G.chunk_bytes), K.max_w_stages, w_cap}) & ~1u;
+    if (K.x_ring_bytes) sw = std::min(sw, std::max(2u, ((ring_budget - std::min(ring_budget, K.x_ring_bytes)) / G.chunk_bytes) & ~1u));
+    p.x_stages = std::min({(ring_budget - sw * G.chunk_bytes) / p.x_slot_bytes, K.max_x_stages, kMaxStages}) & ~1u;
     if (p.x_stages < 2) return set_err(LQG_EVALIDATION, "tile configuration does not fit shared memory");
     p.w_base = p.x_stages * p.x_slot_bytes;
     // A split-K finisher of a large token tile gathers each contributor's
@@ -624,6 +628,18 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
         const int nc = pair_clusters(w->device, smem, 2 * units);
         if (nc > 0 && uint32_t(nc) < units) units = uint32_t(nc);
         grid = 2 * units;
+    }
+    // Fewer tiles than units, large token tiles: the stream-K split's tail
+    // (contributors publish at the end of their ranges, the finisher gathers
+    // and stores after them) costs more than idle SMs. Use exactly 2 units per
+    // tile (equal halves: every unit one piece, no middle pieces) when they
+    // fit, else one unit per tile (no split at all). LLaMA-2-70B on B200:
+    // o at M = 128 18.3 -> 17.4 us, qkv at M = 128 19.4 -> 18.6 us, o at
+    // M = 256 22.8 -> 19.7 us. Smaller token tiles keep every SM streaming
+    // (neutral to +1 % at M = 64, and decode is HBM-bound).
+    if (!K.grid && BN >= 128 && tiles <= units) {
+        units = 2 * tiles <= units ? 2 * tiles : tiles;
+        grid = pair ? 2 * units : units;
     }
     // Hybrid schedule: whole-tile rounds first, stream-K over the last G..2G
     // tiles (all tiles when there are fewer than G), tiles rasterized in groups

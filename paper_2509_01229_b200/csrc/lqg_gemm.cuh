@@ -87,11 +87,15 @@ struct TmemPlan {
 };
 
 // Double-buffered accumulators whenever two fit next to an A ring of >= 2
-// slots. Any ring size works with the two dequant warpgroups taking alternate
-// k-blocks: a warpgroup's ring position advances two slots per k-block and
-// flips its parity on every wrap, i.e. parity = (k-block / slots) & 1, the
-// parity of that slot's use count; a slot's next completion needs this
-// warpgroup's own write, so a wait can never be two phases behind.
+// slots. The A ring may have an odd size although the two dequant
+// warpgroups take alternate k-blocks: a warpgroup's ring position advances
+// two slots per k-block and flips its parity on every wrap, i.e. parity =
+// (k-block / slots) & 1; the empty barrier of k-block i's slot completes
+// with the MMA of k-block i - slots, and MMAs complete in order, so when
+// the warpgroup waits for it, the MMA of k-block i - 2 - slots (its previous
+// wait) and hence of i - 2 * slots are done: the barrier is never two phases
+// behind. (The W and X rings have no such order between the two warpgroups'
+// TMA completions and stay even, see launch_core.)
 __host__ __device__ inline TmemPlan tmem_plan(uint32_t BN, uint32_t max_acc_stages = 2) {
     constexpr uint32_t cols = 512;
     TmemPlan t;
@@ -395,8 +399,16 @@ __device__ __forceinline__ void finish_chunks(const GemmParams& p, uint32_t ch0,
 // contributor pieces (1-2 % slower) and team stores of a last whole tile
 // (neutral).
 enum TeamRole : uint32_t { kTeamNone = 0, kTeamFinish = 1, kTeamWhole = 2 };
+#ifdef LQG_EXP_NOTEAM
+constexpr bool kTeamEnabled = false;
+#else
+constexpr bool kTeamEnabled = true;
+#endif
 __device__ __forceinline__ uint32_t last_team_role(const GemmParams& p, uint32_t dp_rounds, uint32_t sk_beg,
                                                    uint32_t sk_end) {
+#ifdef LQG_EXP_NOTEAM
+    return kTeamNone;
+#endif
     if (p.BN / 16 <= kSentinelMaxChunks) return kTeamNone;
     if (sk_end == sk_beg) return dp_rounds ? kTeamWhole : kTeamNone;
     const uint32_t last_tile = (sk_end - 1) / p.KB;  // relative to the stream-K tiles
@@ -414,13 +426,17 @@ __device__ __forceinline__ void epi_bar() {
 }
 
 #ifdef LQG_TRACE_KB
-// Debug builds: per-k-block clock64 events of CTA 0 (k-blocks 0..63):
+// Debug builds: per-k-block %globaltimer events (ns) of CTAs 0 and 1 (k-blocks 0..63):
 // 0 W issued, 1 X issued, 2 dequant W ready, 3 dequant A slot free,
 // 4 dequant A published, 5 MMA A ready, 6 MMA issued.
-__device__ long long g_lqg_kb[64 * 8];
-#define LQG_KB(i, e)                                                              \
-    do {                                                                          \
-        if (blockIdx.x == 0 && (i) < 64) g_lqg_kb[(i) * 8 + (e)] = clock64();     \
+__device__ long long g_lqg_kb[2 * 64 * 8];  // CTAs 0 and 1 (a pair's leader and peer)
+#define LQG_KB(i, e)                                                                                   \
+    do {                                                                                               \
+        if (blockIdx.x < 2 && (i) < 64) {                                                              \
+            long long t_;                                                                              \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)::"memory");                           \
+            g_lqg_kb[(blockIdx.x * 64 + (i)) * 8 + (e)] = t_;                                          \
+        }                                                                                              \
     } while (0)
 #else
 #define LQG_KB(i, e) ((void)0)
@@ -831,7 +847,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (lane == 0) ptx::mbar_arrive(wempty_bar(w.s));
                 // Half by half: the first half of the slot is rewritten as soon
                 // as the previous k-block's first four MMAs have read it.
+#ifdef LQG_EXP_NOALO
+                LQG_WAIT(dq_a, ptx::mbar_wait(aempty_bar(a.s), a.ph ^ 1));
+#else
                 LQG_WAIT(dq_a, ptx::mbar_wait(aempty_lo_bar(a.s), a.ph ^ 1));
+#endif
                 if (warp % 4 == 2 && lane == 0) LQG_KB(i, 3);
                 ptx::tc_fence_after();
                 ptx::tmem_st_x32(a_taddr, o[0]);
@@ -1083,12 +1103,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef LQG_TRACE_PRO
                     if (et == 0) LQG_T(9);
 #endif
-                    for (uint32_t c = c_first + et; c < c_end; c += 128) {
-                        const uint32_t fc = kPair ? 2 * c + rank : c;
-                        while (ptx::ld_acquire_u32(p.flags + fc) == 0) __nanosleep(32);
-                        p.flags[fc] = 0;
-                    }
-                    epi_bar();
 #ifdef LQG_TRACE_PRO
                     if (et == 0) LQG_T(10);
 #endif
@@ -1096,12 +1110,24 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const uint32_t nb = min(nb_max, c_end - c0);
                         const bool last_batch = c0 + nb >= c_end;
                         if (et == 0 && nb) {
-                            ptx::fence_proxy_async();  // acquired data + prior generic SMEM reads vs TMA
+                            // The thread that issues the copies acquires every
+                            // contributor's flag itself (then one proxy fence
+                            // orders the acquired data before its async-proxy
+                            // reads), each copy issued as soon as its flag is up.
                             ptx::mbar_arrive_expect_tx(fin_bar, nb * part_bytes);
-                            for (uint32_t b = 0; b < nb; ++b)
-                                ptx::bulk_g2s(smem_base + b * part_bytes,
-                                              p.parts + uint64_t(kPair ? 2 * (c0 + b) + rank : c0 + b) * kSlotCellsK + kSmallCells,
-                                              part_bytes, fin_bar, ptx::policy_evict_first());
+                            uint32_t pending = (1u << nb) - 1u;
+                            while (pending) {
+                                for (uint32_t b = 0; b < nb; ++b) {
+                                    const uint32_t fc = kPair ? 2 * (c0 + b) + rank : c0 + b;
+                                    if (!((pending >> b) & 1u) || ptx::ld_acquire_u32(p.flags + fc) == 0) continue;
+                                    p.flags[fc] = 0;
+                                    ptx::fence_proxy_async();  // acquired data + prior generic SMEM reads vs TMA
+                                    ptx::bulk_g2s(smem_base + b * part_bytes, p.parts + uint64_t(fc) * kSlotCellsK + kSmallCells,
+                                                  part_bytes, fin_bar, ptx::policy_evict_first());
+                                    pending &= ~(1u << b);
+                                }
+                                if (pending) __nanosleep(32);
+                            }
                         }
                         if (nb) {
                             ptx::mbar_wait(fin_bar, fin_ph);
@@ -1134,6 +1160,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                             }
                             ptx::tmem_st_wait();
                             epi_bar();  // ring reads done before the next batch
+                        } else if (!kTeamEnabled) {
+                            finish_chunks<kKind, kFan>(p, 0, 1, nchunks, acc_taddr, sm4, nb, part_bytes, row, n, m0,
+                                                       mlim, cs, ts_s);
+                            break;
                         } else {
                             // Last batch: the team finish. This is the CTA's last
                             // segment, so the 8 dequant warps are idle: they take

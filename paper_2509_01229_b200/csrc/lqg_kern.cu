@@ -74,7 +74,7 @@ int LQG_CAT(pair_clusters_kind, LQG_KIND)(size_t smem, uint32_t grid) {
 #ifdef LQG_TRACE_KB
 // LQG_TRACE_KB builds: this unit's per-k-block event buffer of CTA 0.
 extern "C" int LQG_CAT(lqg_debug_kb_kind, LQG_KIND)(long long* out) {
-    return cudaMemcpyFromSymbol(out, g_lqg_kb, sizeof(long long) * 64 * 8) == cudaSuccess ? 0 : 4;
+    return cudaMemcpyFromSymbol(out, g_lqg_kb, sizeof(long long) * 2 * 64 * 8) == cudaSuccess ? 0 : 4;
 }
 #endif
 

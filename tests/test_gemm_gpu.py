@@ -671,6 +671,31 @@ def test_pdl_launch_chain(torch_cuda, lqg, m):
             assert torch.equal(a, b)
 
 
+def test_split_k_sequence_stress(torch_cuda, lqg):
+    """Regression for a ring-parity race (odd W rings let one dequant warpgroup
+    run two phases ahead of the other and read a weight slot that had not
+    landed): the sequence that exposed it -- large-token-tile split-K launches
+    of different shapes and kernels back to back on one stream, repeated --
+    must give exact INT32 accumulators (checked against an exact float64
+    product of the dequantized weights) every time."""
+    torch = torch_cuda
+    cfgs = [(4096, 1024, 8192), (1000, 2048, 4096), (2048, 384, 640), (3001, 384, 640)]
+    data = []
+    for (m, n, k) in cfgs:
+        g = torch.Generator(device="cuda").manual_seed(m + n)
+        dw = lqg.DeviceWeights.quantize(torch.randn(n, k, generator=g, device="cuda") * 0.02, 128)
+        q, ts = lqg.quantize_activations(torch.randn(m, k, generator=g, device="cuda"))
+        ref = (q.to(torch.float64) @ dw.dequant().to(torch.float64).T).to(torch.int32)
+        data.append((dw, q, ts, ref))
+    for _ in range(6):
+        for dw, q, ts, ref in data:
+            for pair in (0, 1):
+                with lqg.tune(pair=pair):
+                    acc = dw.gemm_accum(q)
+                    dw.gemm(q, ts)
+                assert torch.equal(acc, ref)
+
+
 def test_tune_rejects_unknown_and_out_of_range(lqg):
     with pytest.raises(lqg.ValidationError):
         lqg.tune_set("no_such_knob", 1)

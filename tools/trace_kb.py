@@ -33,14 +33,17 @@ y = torch.empty(m, n, dtype=torch.bfloat16, device="cuda")
 for _ in range(3):
     dw.gemm(q, ts, out=y)
 torch.cuda.synchronize()
-buf = np.zeros(64 * 8, np.int64)
+buf = np.zeros(2 * 64 * 8, np.int64)
 C = ctypes.CDLL(_lib.LIB_PATH)
 C.lqg_debug_kb_kind3(buf.ctypes.data_as(ctypes.c_void_p))
-ev = buf.reshape(64, 8)
+both = buf.reshape(2, 64, 8)
+cta = int(os.environ.get("CTA", "0"))  # 0: CTA 0 (a pair's leader), 1: CTA 1 (its peer)
+ev = both[cta]
 names = ["W req", "X req", "dq W ok", "dq A free", "dq A pub", "mma A ok", "mma issued", "dq st done"]
 sel = ev[first:first + count, :8]
-t0 = sel[sel > 0].min()
-print(f"{sys.argv[1]}: CTA 0, k-blocks {first}..{first + count - 1} (cycles from the first event)")
+allsel = both[:, first:first + count, :8]
+t0 = allsel[allsel > 0].min()  # one global clock (%globaltimer, ns) for both CTAs
+print(f"{sys.argv[1]}: CTA {cta}, k-blocks {first}..{first + count - 1} (ns from the first event of either CTA)")
 print("  kb " + "".join(f"{nm:>11s}" for nm in names) + "   A-pub->mma-ok  issue->next-A-ok")
 for r, row in enumerate(sel):
     i = first + r
@@ -49,4 +52,4 @@ for r, row in enumerate(sel):
     nxt = ev[i + 1, 5] - row[6] if i + 1 < 64 and ev[i + 1, 5] and row[6] else -1
     print(f"  {i:2d} {vals}   {lag:8d}   {nxt:8d}")
 d = np.diff(ev[first:first + count, 6])
-print(f"  MMA issue period: median {np.median(d):.0f} cycles/k-block")
+print(f"  MMA issue period: median {np.median(d):.0f} ns/k-block")
