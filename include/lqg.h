@@ -239,7 +239,9 @@ uint64_t lqg_kernel_launch_count(void);
 /* Launch-schedule knobs (tuning and testing hook, process-wide): token-tile
  * cap "max_bn", CTA pairs "pair" (-1 auto, 0 never, 1 wherever legal),
  * "pair_min_m", "pair_single_tile", ring split "x_ring_bytes",
- * "max_x_stages", "max_w_stages", "grid", "raster_gm", "no_dp", "no_pdl".
+ * "max_x_stages", "max_w_stages" (ring depths are rounded down to even),
+ * "grid", "raster_gm", "no_dp", "no_pdl", "acc_stages" (1: one accumulator
+ * stage and a deeper TMEM A ring).
  * Results are bit-identical under every setting; only the schedule changes.
  * Unknown names and out-of-range values -> LQG_EVALIDATION. */
 int lqg_tune_set(const char* name, int64_t value);

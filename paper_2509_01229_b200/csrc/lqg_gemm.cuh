@@ -140,7 +140,7 @@ struct GemmParams {
 // token scales of the current tile (double).
 constexpr uint32_t kMiscTsOff = 128;
 constexpr uint32_t kMiscBytes = kMiscTsOff + kMaxBN * 8;
-constexpr uint32_t kNumBarriers = 4 * kMaxStages + 3 * kMaxASlots + 7;
+constexpr uint32_t kNumBarriers = 4 * kMaxStages + 3 * kMaxASlots + 8;
 
 // Grouped launch (MoE experts of one layer: same n, k, group size): the
 // tiles of every group form one linear space, tile-major within a group.
@@ -508,7 +508,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     // first half of an A slot (K columns 0..127) read: the MMA warp commits after
     // the k-block's first four MMAs
     auto aempty_lo_bar = [&](uint32_t a) { return bar_base + 8 * (kB + 2 * kMaxASlots + 7 + a); };
-    uint8_t* misc = smem + ((ring_bytes + 7) & ~7u) + 8 * (kB + 3 * kMaxASlots + 7);
+    // every dequant warp has finished reading the W ring (the finisher's
+    // gather reuses the rings; the order also runs through the MMA, this
+    // makes it explicit)
+    const uint32_t dq_done = bar_base + 8 * (kB + 3 * kMaxASlots + 7);
+    uint8_t* misc = smem + ((ring_bytes + 7) & ~7u) + 8 * (kB + 3 * kMaxASlots + 8);
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(misc);
     double* ts_s = reinterpret_cast<double*>(misc + kMiscTsOff);  // kMaxBN token scales, as double
     uint32_t* team_info = reinterpret_cast<uint32_t*>(misc + 64);  // team finish: tile, acc column, nb
@@ -546,6 +550,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_init(fin_bar, 1);
             ptx::mbar_init(team_ready, 1);         // the epilogue's leading thread
             ptx::mbar_init(team_done, kDQWarps);   // one arrive per dequant warp
+            ptx::mbar_init(dq_done, kDQWarps);
         }
         ptx::fence_mbar_init();
     }
@@ -887,6 +892,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             case 4: run(UConst<4>{}); break;
             default: run(UConst<8>{}); break;
         }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(dq_done);
         // Team finish (see the epilogue's large finisher): the last batch's
         // reduction and stores of chunks 1 + wg, 4 + wg, ... of the
         // finisher tile, once the epilogue warps have gathered it.
@@ -1110,6 +1117,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const uint32_t nb = min(nb_max, c_end - c0);
                         const bool last_batch = c0 + nb >= c_end;
                         if (et == 0 && nb) {
+                            ptx::mbar_wait(dq_done, 0);  // the W ring's last reads are done
                             // The thread that issues the copies acquires every
                             // contributor's flag itself (then one proxy fence
                             // orders the acquired data before its async-proxy
