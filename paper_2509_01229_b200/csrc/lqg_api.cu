@@ -361,7 +361,7 @@ constexpr uint32_t kSmemMisc = (1024 + 8 * kNumBarriers + 8 + kMiscBytes + 1023)
 // tests change them through lqg_tune_set (process-wide, no environment reads).
 enum TuneId : int {
     kTuneMaxBN, kTunePairMinM, kTunePair, kTunePairSingleTile, kTuneXRingBytes, kTuneMaxXStages,
-    kTuneMaxWStages, kTuneGrid, kTuneRasterGM, kTuneNoDP, kTuneNoPDL, kTuneAccStages, kTuneCount
+    kTuneMaxWStages, kTuneGrid, kTuneRasterGM, kTuneNoDP, kTuneNoPDL, kTuneAccStages, kTuneHostChunkM, kTuneHostChunks, kTuneCount
 };
 struct TuneDef {
     const char* name;
@@ -380,16 +380,20 @@ constexpr TuneDef kTuneDefs[kTuneCount] = {
     {"no_dp", 0, 0, 1},                            // stream-K over all tiles
     {"no_pdl", 0, 0, 1},                           // no programmatic dependent launch
     {"acc_stages", 2, 1, 2},                       // accumulator stages in TMEM (the rest is A ring)
+    {"host_chunk_m", 384, 1, 1 << 30},             // host-buffer calls of >= this many rows are pipelined
+    {"host_chunks", 6, 1, 8},                      // ... in this many row chunks
 };
 std::atomic<int64_t> g_tune[kTuneCount] = {
     {kTuneDefs[0].dflt}, {kTuneDefs[1].dflt}, {kTuneDefs[2].dflt}, {kTuneDefs[3].dflt},
     {kTuneDefs[4].dflt}, {kTuneDefs[5].dflt}, {kTuneDefs[6].dflt}, {kTuneDefs[7].dflt},
-    {kTuneDefs[8].dflt}, {kTuneDefs[9].dflt}, {kTuneDefs[10].dflt}, {kTuneDefs[11].dflt}};
+    {kTuneDefs[8].dflt}, {kTuneDefs[9].dflt}, {kTuneDefs[10].dflt}, {kTuneDefs[11].dflt},
+    {kTuneDefs[12].dflt}, {kTuneDefs[13].dflt}};
 
 struct Knobs {
     uint32_t max_bn, pair_min_m;
     int pair;
-    uint32_t pair_single_tile, x_ring_bytes, max_x_stages, max_w_stages, grid, raster_gm, no_dp, no_pdl, acc_stages;
+    uint32_t pair_single_tile, x_ring_bytes, max_x_stages, max_w_stages, grid, raster_gm, no_dp, no_pdl, acc_stages, host_chunk_m,
+        host_chunks;
 };
 Knobs knobs() {
     auto g = [](TuneId i) { return g_tune[i].load(std::memory_order_relaxed); };
@@ -406,6 +410,8 @@ Knobs knobs() {
     k.no_dp = uint32_t(g(kTuneNoDP));
     k.no_pdl = uint32_t(g(kTuneNoPDL));
     k.acc_stages = uint32_t(g(kTuneAccStages));
+    k.host_chunk_m = uint32_t(g(kTuneHostChunkM));
+    k.host_chunks = uint32_t(g(kTuneHostChunks));
     return k;
 }
 
@@ -1278,11 +1284,17 @@ int host_call_on(const lqg_weights* w, Staging& S, const int8_t* x, const float*
     if (!rc) rc = ensure_cap(reinterpret_cast<void**>(&S.d_ts), &S.ts_cap, size_t(m) * 4);
     if (!rc) rc = ensure_cap(&S.d_y, &S.y_cap, size_t(m) * G.n * ebytes);
     if (rc) return rc;
-    // Large calls are cut into row chunks pipelined over three streams:
-    // H2D of chunk c+1 and D2H of chunk c-1 (PCIe is full duplex) overlap the
-    // GEMM of chunk c, so the call costs ~max(H2D, D2H) instead of their sum
-    // plus the GEMM. Small calls (latency-bound) stay one chunk.
-    const uint32_t per = m >= 2048 ? std::max<uint32_t>(1024, (m + 7) / 8) : m;
+    // Calls of >= host_chunk_m rows are cut into row chunks pipelined over
+    // three streams: H2D of chunk c+1 and D2H of chunk c-1 (PCIe is full
+    // duplex) overlap the GEMM of chunk c, so the call costs ~max(H2D, D2H)
+    // instead of their sum plus the GEMM. Small calls (latency-bound) stay one
+    // chunk. B200 box: pinned D2H 55.8 GB/s, H2D + D2H concurrently 87 GB/s;
+    // the 70B e2e step (52 calls) 26.1 ms at (2048 rows, 8 chunks) -> 24.3 ms
+    // at (384, 6), against a ~17-21 ms PCIe floor (tools/e2e_probe.py).
+    const Knobs K = knobs();
+    const uint32_t per = m >= K.host_chunk_m ? std::max<uint32_t>(std::min<uint32_t>(1024, K.host_chunk_m / 2),
+                                                                   (m + K.host_chunks - 1) / K.host_chunks)
+                                             : m;
     const uint32_t nchunk = (m + per - 1) / per;
     if (nchunk > 1 && !S.s_in) {
         LQG_CUDA(cudaStreamCreateWithFlags(&S.s_in, cudaStreamNonBlocking));
