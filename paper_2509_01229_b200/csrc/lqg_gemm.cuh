@@ -399,16 +399,9 @@ __device__ __forceinline__ void finish_chunks(const GemmParams& p, uint32_t ch0,
 // contributor pieces (1-2 % slower) and team stores of a last whole tile
 // (neutral).
 enum TeamRole : uint32_t { kTeamNone = 0, kTeamFinish = 1, kTeamWhole = 2 };
-#ifdef LQG_EXP_NOTEAM
-constexpr bool kTeamEnabled = false;
-#else
-constexpr bool kTeamEnabled = true;
-#endif
+
 __device__ __forceinline__ uint32_t last_team_role(const GemmParams& p, uint32_t dp_rounds, uint32_t sk_beg,
                                                    uint32_t sk_end) {
-#ifdef LQG_EXP_NOTEAM
-    return kTeamNone;
-#endif
     if (p.BN / 16 <= kSentinelMaxChunks) return kTeamNone;
     if (sk_end == sk_beg) return dp_rounds ? kTeamWhole : kTeamNone;
     const uint32_t last_tile = (sk_end - 1) / p.KB;  // relative to the stream-K tiles
@@ -604,11 +597,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         const uint8_t* src = chunk_src(ww.tile, ww.kb);
         RingPos w{0, 0};
-#ifdef LQG_EXP_MMAONLY
-        for (uint32_t i = 0; i < 0; ++i) {
-#else
         for (uint32_t i = 0; i < n_local; ++i) {
-#endif
             ptx::mbar_wait(wempty_bar(w.s), w.ph ^ 1);
             if (ptx::elect_one()) {
                 ptx::mbar_arrive_expect_tx(wfull_bar(w.s), p.chunk_bytes);
@@ -634,12 +623,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         RingPos x{0, 0};
         for (uint32_t i = 0; i < n_local; ++i) {
             ptx::mbar_wait(xempty_bar(x.s), x.ph ^ 1);
-#if defined(LQG_EXP_NOX) || defined(LQG_EXP_MMAONLY)  // timing experiments only: no activation loads (garbage B)
-            if (ptx::elect_one() && (!kPair || rank == 0)) ptx::mbar_arrive(xfull_bar(x.s));
-            if (false) {
-#else
             if (ptx::elect_one()) {
-#endif
                 const uint32_t slot = smem_base + x.s * p.x_slot_bytes;
                 const int32_t k0 = int32_t(xw.kb * kKBlock);
                 if (kPair) {
@@ -685,9 +669,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
         auto wait_ready = [&]() {
             if (seg_start) LQG_WAIT(w_acc, ptx::mbar_wait(accempty_bar(as), acc_ph ^ 1));
-#ifndef LQG_EXP_NOAWAIT  // timing experiment: MMA does not wait for the dequant (garbage A)
             LQG_WAIT(w_a, ptx::mbar_wait(afull_bar(a.s), a.ph));
-#endif
             ptx::tc_fence_after();
         };
         auto mma = [&](uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t k8, bool first) {
@@ -781,19 +763,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                 xr.adv(2, SX);
             };
             for (uint32_t i = wg; i < n_local; i += 2) {
-#ifdef LQG_EXP_MMAONLY
-                ptx::mbar_wait(aempty_bar(a.s), a.ph ^ 1);
-                wait_x();
-                __syncwarp();
-                if (lane == 0) {
-                    if (kPair && rank != 0)
-                        ptx::mbar_arrive_cluster_relaxed(leader(afull_bar(a.s)));
-                    else
-                        ptx::mbar_arrive(afull_bar(a.s));
-                }
-                a.adv(2, tp.a_slots);
-                continue;
-#endif
                 LQG_WAIT(dq_w, ptx::mbar_wait(wfull_bar(w.s), w.ph));
                 if (warp % 4 == 2 && lane == 0) LQG_KB(i, 2);
                 const uint8_t* wchunk = wring + w.s * p.chunk_bytes;
@@ -823,14 +792,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                     a4 = (sa >> 8) * 0x01010101u;
                 };
                 uint4 v[kSubBlocks];
-#ifdef LQG_EXP_NODQ  // timing experiment only: no code loads (garbage A)
-#pragma unroll
-                for (uint32_t c = 0; c < kSubBlocks; ++c) v[c] = make_uint4(row, c, i, prm[0]);
-#else
 #pragma unroll
                 for (uint32_t c = 0; c < kSubBlocks; ++c)
                     v[c] = *reinterpret_cast<const uint4*>(wchunk + (c * kTileN + row) * 16);
-#endif
                 // The whole k-block is converted before the A slot is claimed, so
                 // once the MMA frees the slot only the two TMEM stores stand
                 // between it and the next afull arrival (two A slots per
@@ -852,11 +816,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (lane == 0) ptx::mbar_arrive(wempty_bar(w.s));
                 // Half by half: the first half of the slot is rewritten as soon
                 // as the previous k-block's first four MMAs have read it.
-#ifdef LQG_EXP_NOALO
-                LQG_WAIT(dq_a, ptx::mbar_wait(aempty_bar(a.s), a.ph ^ 1));
-#else
                 LQG_WAIT(dq_a, ptx::mbar_wait(aempty_lo_bar(a.s), a.ph ^ 1));
-#endif
                 if (warp % 4 == 2 && lane == 0) LQG_KB(i, 3);
                 ptx::tc_fence_after();
                 ptx::tmem_st_x32(a_taddr, o[0]);
@@ -979,11 +939,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (small) load_batch(c_first, 0);
             }
             epi_bar();
-#ifdef LQG_EXP_SPINACC
-            ptx::mbar_wait(accfull_bar(as), acc_ph);
-#else
             ptx::mbar_wait_parked(accfull_bar(as), acc_ph);  // idle for a tile mainloop
-#endif
             if (i >= n_local && et == 0) LQG_T(6);
             ptx::tc_fence_after();
             const uint32_t acc_taddr = tmem_base + lane_addr + as * tp.acc_stride;
@@ -1168,10 +1124,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                             }
                             ptx::tmem_st_wait();
                             epi_bar();  // ring reads done before the next batch
-                        } else if (!kTeamEnabled) {
-                            finish_chunks<kKind, kFan>(p, 0, 1, nchunks, acc_taddr, sm4, nb, part_bytes, row, n, m0,
-                                                       mlim, cs, ts_s);
-                            break;
                         } else {
                             // Last batch: the team finish. This is the CTA's last
                             // segment, so the 8 dequant warps are idle: they take
