@@ -435,6 +435,29 @@ __device__ long long g_lqg_kb[2 * 64 * 8];  // CTAs 0 and 1 (a pair's leader and
 #define LQG_KB(i, e) ((void)0)
 #endif
 
+#ifdef LQG_TRACE_SEG
+// Debug builds: per-segment (accumulator stage use) %globaltimer events of CTAs
+// 0..7, segments 0..31: 0 MMA starts waiting for the stage, 1 stage free,
+// 2 last MMA of the segment issued, 3 epilogue sees the accumulator, 4 stage
+// released, 5 epilogue segment done, 6 k-blocks in the segment, 7 kind (0 whole
+// tile, 1 contributor, 2 finisher), 8 / 9 whole tile: epilogue warp 10's
+// cycles in TMEM load + wait / in scale + store.
+__device__ long long g_lqg_seg[8 * 32 * 16];
+#define LQG_SEG(j, e, v)                                                                        \
+    do {                                                                                        \
+        if (blockIdx.x < 8 && (j) < 32) g_lqg_seg[(blockIdx.x * 32 + (j)) * 16 + (e)] = (v);   \
+    } while (0)
+#define LQG_SEGT(j, e)                                                          \
+    do {                                                                        \
+        long long t_;                                                           \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)::"memory");        \
+        LQG_SEG(j, e, t_);                                                      \
+    } while (0)
+#else
+#define LQG_SEG(j, e, v) ((void)0)
+#define LQG_SEGT(j, e) ((void)0)
+#endif
+
 #ifdef LQG_TRACE
 // Debug builds: per-CTA %globaltimer events and per-role wait cycles.
 __device__ unsigned long long g_lqg_trace[8 * 160 * 16];
@@ -663,12 +686,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         bool seg_start = true;
         RingPos x{0, 0}, a{0, 0};
         uint32_t as = 0, acc_ph = 0;
+#ifdef LQG_TRACE_SEG
+        uint32_t sidx = 0;
+#endif
 #ifdef LQG_TRACE
         long long w_acc = 0, w_a = 0, w_x = 0, w_issue = 0;  // w_x: unused (X folded into afull)
         const long long t_mma0 = clock64();
 #endif
         auto wait_ready = [&]() {
-            if (seg_start) LQG_WAIT(w_acc, ptx::mbar_wait(accempty_bar(as), acc_ph ^ 1));
+            if (seg_start) {
+                if (lane == 0) LQG_SEGT(sidx, 0);
+                LQG_WAIT(w_acc, ptx::mbar_wait(accempty_bar(as), acc_ph ^ 1));
+                if (lane == 0) LQG_SEGT(sidx, 1);
+            }
             LQG_WAIT(w_a, ptx::mbar_wait(afull_bar(a.s), a.ph));
             ptx::tc_fence_after();
         };
@@ -709,11 +739,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 commit(xempty_bar(x.s));
                 commit(aempty_bar(a.s));
                 if (seg_end) commit(accfull_bar(as));
+                if (seg_end) LQG_SEGT(sidx, 2);
                 LQG_KB(i, 6);
             }
             __syncwarp();
 #ifdef LQG_TRACE
             w_issue += clock64() - t_is0;
+#endif
+#ifdef LQG_TRACE_SEG
+            if (seg_end) ++sidx;
 #endif
             if (seg_end && ++as == tp.acc_stages) {
                 as = 0;
@@ -884,7 +918,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t i = 0;
         Walk ew;
         ew.init(sch);
+#ifdef LQG_TRACE_SEG
+        uint32_t eidx = 0;
+#endif
         auto release_acc = [&](uint32_t cur_as) {
+            if (et == 0) LQG_SEGT(eidx, 4);
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) {
@@ -940,6 +978,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             epi_bar();
             ptx::mbar_wait_parked(accfull_bar(as), acc_ph);  // idle for a tile mainloop
+            if (et == 0) {
+                LQG_SEGT(eidx, 3);
+                LQG_SEG(eidx, 6, n_iters);
+                LQG_SEG(eidx, 7, n_iters == KB ? 0 : (kb0 > 0 ? 1 : 2));
+            }
             if (i >= n_local && et == 0) LQG_T(6);
             ptx::tc_fence_after();
             const uint32_t acc_taddr = tmem_base + lane_addr + as * tp.acc_stride;
@@ -950,10 +993,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             if (n_iters == KB) {
                 // whole tile: scale, cast and store straight from TMEM
+#ifdef LQG_TRACE_SEG
+                long long c_ld = 0, c_st = 0;
+#endif
                 for (uint32_t ch = 0; ch < nchunks; ++ch) {
                     uint32_t v[16];
+#ifdef LQG_TRACE_SEG
+                    const long long c0 = clock64();
+#endif
                     ptx::tmem_ld_x16(acc_taddr + ch * 16, v);
                     ptx::tmem_ld_wait();
+#ifdef LQG_TRACE_SEG
+                    const long long c1 = clock64();
+                    c_ld += c1 - c0;
+#endif
                     if (ch + 1 == nchunks) release_acc(cur_as);
                     if (n < p.N) {
                         int32_t a[16];
@@ -961,7 +1014,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (uint32_t j = 0; j < 16; ++j) a[j] = int32_t(v[j]);
                         store_chunk_k<kKind, kFan>(p, m0 + ch * 16, mlim, n, a, cs, ts_s + ch * 16);
                     }
+#ifdef LQG_TRACE_SEG
+                    asm volatile("" ::: "memory");
+                    c_st += clock64() - c1;
+#endif
                 }
+#ifdef LQG_TRACE_SEG
+                if (et == 0) {
+                    LQG_SEG(eidx, 8, c_ld);
+                    LQG_SEG(eidx, 9, c_st);
+                }
+#endif
             } else if (kb0 > 0) {
                 // Contributor piece of a split tile (always this CTA's first
                 // segment): publish the INT32 partial into this CTA's cells.
@@ -1153,6 +1216,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 release_acc(cur_as);
             }
             epi_bar();  // ts_s reuse
+#ifdef LQG_TRACE_SEG
+            if (et == 0) LQG_SEGT(eidx, 5);
+            ++eidx;
+#endif
         }
 #ifdef LQG_TRACE_PRO
         if (et == 0) LQG_T(13);

@@ -78,6 +78,13 @@ extern "C" int LQG_CAT(lqg_debug_kb_kind, LQG_KIND)(long long* out) {
 }
 #endif
 
+#ifdef LQG_TRACE_SEG
+// LQG_TRACE_SEG builds: this unit's per-segment event buffer of CTAs 0..7.
+extern "C" int LQG_CAT(lqg_debug_seg_kind, LQG_KIND)(long long* out) {
+    return cudaMemcpyFromSymbol(out, g_lqg_seg, sizeof(long long) * 8 * 32 * 16) == cudaSuccess ? 0 : 4;
+}
+#endif
+
 // LQG_TRACE builds: this unit's per-CTA event buffer (zeros otherwise).
 int LQG_CAT(debug_trace_kind, LQG_KIND)(unsigned long long* out) {
 #ifdef LQG_TRACE

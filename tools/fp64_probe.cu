@@ -3,7 +3,31 @@
 // as the FP32 reference. 8 independent chains per thread, grid = 4 x SMs.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 tools/fp64_probe.cu -o tools/fp64_probe.bin
 #include <cuda_runtime.h>
+#include <cstdint>
 #include <cstdio>
+
+// The FP32 alternative measured in round 2 (rejected): the
+// reference's float(double(acc) * cs * ts) from a TwoProduct split of acc*cs
+// and an FMA, exact unless the result lies within 2^-19 half-ulp of a float
+// rounding midpoint (then the double chain).
+__device__ __forceinline__ int lqs_scale_f32(int32_t acc, float cs, float ts, float* out) {
+    const int small = (uint32_t)(acc + 0x400000) < 0x800000u;
+    const float A = __fadd_rn(__uint_as_float(0x4B400000u + (uint32_t)acc), -12582912.0f);
+    const float hi = __fmul_rn(A, cs);
+    const float lo = __fmaf_rn(A, cs, -hi);
+    const float t = __fmul_rn(lo, ts);
+    const float r = __fmaf_rn(hi, ts, t);
+    const float d = __fadd_rn(__fmaf_rn(hi, ts, -r), t);
+    const float p2 = __uint_as_float(__float_as_uint(r) & 0x7F800000u);
+    const float ahi = fabsf(hi);
+    const float hu = __fmul_rn(p2, 0x1p-24f), tol = __fmul_rn(p2, 0x1p-43f);
+    *out = r;
+    return small & (p2 >= 0x1p-80f) & (p2 < 0x1p126f) & (ahi >= 0x1p-80f) & (ahi < 0x1p126f) &
+           (fabsf(__fadd_rn(fabsf(d), -hu)) > tol);
+}
+__device__ __forceinline__ float lqs_scale_f64(int32_t acc, double cs_d, float ts) {
+    return __double2float_rn(__dmul_rn(__dmul_rn(double(acc), cs_d), double(ts)));
+}
 
 constexpr int kIters = 4096;
 
@@ -61,17 +85,58 @@ __global__ void k_fmul(double* out, double s) {
     if (r == 1.2345f) out[0] = r;
 }
 
+// the epilogue's per-output chain, 8 outputs per thread per iteration:
+// int32 -> double (DADD trick), two DMUL, F2F.F32.F64 (the reference chain) ...
+__global__ void k_chain64(double* out, double s) {
+    const double cs = 0.0123 * s, ts = 0.031;
+    float acc = 0.f;
+    for (int it = 0; it < kIters; ++it)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int a = int(threadIdx.x * 977 + it * 131 + i * 7919) - 300000;
+            const double d = __hiloint2double(0x43300000, int(uint32_t(a) ^ 0x80000000u)) - 4503601774854144.0;
+            acc += __double2float_rn(__dmul_rn(__dmul_rn(d, cs), ts));
+        }
+    if (acc == 1.2345f) out[0] = acc;
+}
+// ... and the FP32 fast path of lqg_scale.h (fallbacks counted in out[1])
+__global__ void k_chain32(double* out, double s) {
+    const float cs = float(0.0123 * s), ts = 0.031f;
+    float acc = 0.f;
+    unsigned slow_n = 0;
+    for (int it = 0; it < kIters; ++it) {
+        unsigned slow = 0;
+        float y[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int a = int(threadIdx.x * 977 + it * 131 + i * 7919) - 300000;
+            slow |= lqs_scale_f32(a, cs, ts, &y[i]) ? 0u : (1u << i);
+        }
+        if (slow) {
+            slow_n += __popc(slow);
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                if ((slow >> i) & 1u) y[i] = lqs_scale_f64(int(threadIdx.x * 977 + it * 131 + i * 7919) - 300000, double(cs), ts);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc += y[i];
+    }
+    if (acc == 1.2345f) out[0] = acc;
+    if (slow_n) atomicAdd(reinterpret_cast<unsigned long long*>(out) + 1, (unsigned long long)slow_n);
+}
+
 int main() {
     int sms, clk;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
     double* out;
-    cudaMalloc(&out, 8);
+    cudaMalloc(&out, 16);
+    cudaMemset(out, 0, 16);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    auto run = [&](const char* name, void (*k)(double*, double)) {
-        const int blocks = 4 * sms, threads = 256;
+    auto run = [&](const char* name, void (*k)(double*, double), int blocks_per_sm = 4, int threads = 256) {
+        const int blocks = blocks_per_sm * sms;
         k<<<blocks, threads>>>(out, 1.0000001);
         cudaDeviceSynchronize();
         cudaEventRecord(e0);
@@ -89,5 +154,14 @@ int main() {
     run("DMUL+F2F.F32.F64+FADD", k_f2f);
     run("I2F.F64+DADD", k_i2f);
     run("FMUL", k_fmul);
+    // per output (8 per thread-iteration): throughput with 8 warps per SMSP,
+    // then one warp per SMSP (the epilogue's situation)
+    run("epilogue chain FP64", k_chain64);
+    run("epilogue chain FP32 fast path", k_chain32);
+    run("FP64 chain, 1 warp/SMSP", k_chain64, 1, 128);
+    run("FP32 chain, 1 warp/SMSP", k_chain32, 1, 128);
+    unsigned long long nslow = 0;
+    cudaMemcpy(&nslow, out + 1, 8, cudaMemcpyDeviceToHost);
+    printf("fast-path fallbacks: %llu\n", nslow);
     printf("status: %s\n", cudaGetErrorString(cudaGetLastError()));
 }

@@ -16,7 +16,7 @@ import torch
 
 from paper_2509_01229_b200 import _lib
 
-_lib.LIB_PATH = os.path.join(_lib.HERE, "liblqg_tracekb.so")
+_lib.LIB_PATH = os.path.join(_lib.HERE, os.environ.get("TRACE_LIB", "liblqg_tracekb.so"))
 _lib._stale = lambda: False
 import paper_2509_01229_b200 as lqg
 
