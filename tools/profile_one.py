@@ -22,7 +22,11 @@ def main():
     ap.add_argument("--g", type=int, default=128)
     ap.add_argument("--iters", type=int, default=4)
     ap.add_argument("--time", action="store_true")
+    ap.add_argument("--tune", action="append", default=[], help="knob=value (repeatable)")
     a = ap.parse_args()
+    for kv in a.tune:
+        kk, vv = kv.split("=")
+        lqg.tune_set(kk, int(vv))
     torch.manual_seed(0)
     w = torch.randn(a.n, a.k, device="cuda") * 0.02
     dw = lqg.DeviceWeights.quantize(w, a.g)
