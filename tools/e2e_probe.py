@@ -69,3 +69,19 @@ for cfg in (sys.argv[1:] or [""]):
             torch.cuda.synchronize()
             best = min(best, time.perf_counter() - t0)
     print(f"e2e [{cfg or 'default'}]: {best * 1e3:.2f} ms/step = {ops / best / 1e12:.1f} TOPS")
+
+# per-M breakdown of the default configuration: time of the 4 calls, their
+# PCIe bytes, and the effective transfer rate
+print("   M    ms   H2D MB   D2H MB   GB/s (H2D+D2H over the calls' time)")
+for m in ms:
+    best = 1e9
+    for _ in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for name, n, k, dw in layers:
+            qh, th = hx[k]
+            dw.gemm_host(qh[:m], th[:m], hy[name][:m])
+        best = min(best, time.perf_counter() - t0)
+    h2d = sum(m * k + 4 * m for _, n, k, _ in layers)
+    d2h = sum(2 * m * n for _, n, k, _ in layers)
+    print(f"{m:5d} {best * 1e3:6.3f} {h2d / 1e6:8.1f} {d2h / 1e6:8.1f} {(h2d + d2h) / best / 1e9:7.1f}")
