@@ -361,7 +361,7 @@ constexpr uint32_t kSmemMisc = (1024 + 8 * kNumBarriers + 8 + kMiscBytes + 1023)
 // tests change them through lqg_tune_set (process-wide, no environment reads).
 enum TuneId : int {
     kTuneMaxBN, kTunePairMinM, kTunePair, kTunePairSingleTile, kTuneXRingBytes, kTuneMaxXStages,
-    kTuneMaxWStages, kTuneGrid, kTuneRasterGM, kTuneNoDP, kTuneNoPDL, kTuneAccStages, kTuneHostChunkM, kTuneHostChunks, kTuneCount
+    kTuneMaxWStages, kTuneGrid, kTuneRasterGM, kTuneNoDP, kTuneNoPDL, kTuneAccStages, kTuneHostChunkM, kTuneHostChunks, kTuneNoQuad, kTuneCount
 };
 struct TuneDef {
     const char* name;
@@ -382,18 +382,19 @@ constexpr TuneDef kTuneDefs[kTuneCount] = {
     {"acc_stages", 2, 1, 2},                       // accumulator stages in TMEM (the rest is A ring)
     {"host_chunk_m", 384, 1, 1 << 30},             // host-buffer calls of >= this many rows are pipelined
     {"host_chunks", 6, 1, 8},                      // ... in this many row chunks
+    {"no_quad", 0, 0, 1},                          // 1: split tiles exchange through L2 even where a 4-CTA cluster fits
 };
 std::atomic<int64_t> g_tune[kTuneCount] = {
     {kTuneDefs[0].dflt}, {kTuneDefs[1].dflt}, {kTuneDefs[2].dflt}, {kTuneDefs[3].dflt},
     {kTuneDefs[4].dflt}, {kTuneDefs[5].dflt}, {kTuneDefs[6].dflt}, {kTuneDefs[7].dflt},
     {kTuneDefs[8].dflt}, {kTuneDefs[9].dflt}, {kTuneDefs[10].dflt}, {kTuneDefs[11].dflt},
-    {kTuneDefs[12].dflt}, {kTuneDefs[13].dflt}};
+    {kTuneDefs[12].dflt}, {kTuneDefs[13].dflt}, {kTuneDefs[14].dflt}};
 
 struct Knobs {
     uint32_t max_bn, pair_min_m;
     int pair;
     uint32_t pair_single_tile, x_ring_bytes, max_x_stages, max_w_stages, grid, raster_gm, no_dp, no_pdl, acc_stages, host_chunk_m,
-        host_chunks;
+        host_chunks, no_quad;
 };
 Knobs knobs() {
     auto g = [](TuneId i) { return g_tune[i].load(std::memory_order_relaxed); };
@@ -412,6 +413,7 @@ Knobs knobs() {
     k.acc_stages = uint32_t(g(kTuneAccStages));
     k.host_chunk_m = uint32_t(g(kTuneHostChunkM));
     k.host_chunks = uint32_t(g(kTuneHostChunks));
+    k.no_quad = uint32_t(g(kTuneNoQuad));
     return k;
 }
 
@@ -468,16 +470,18 @@ int activation_tmap(const int8_t* d_x, uint32_t k, uint32_t m, int64_t ldx, uint
     return LQG_OK;
 }
 
-// Co-resident 2-CTA clusters for the pair kernel at this shared-memory size
-// (not every SM can host half of a cluster: GPC / TPC boundaries), per device.
-int pair_clusters(int device, size_t smem, uint32_t grid) {
+// Co-resident 2-CTA (or 4-CTA) clusters for the pair kernel at this
+// shared-memory size (not every SM can host part of a cluster: GPC / TPC
+// boundaries), per device.
+int pair_clusters(int device, size_t smem, uint32_t grid, uint32_t cluster = 2) {
     static std::mutex mu;
     static std::vector<std::pair<std::pair<int, size_t>, int>> memo;
+    const size_t key = smem * 8 + cluster;
     std::lock_guard<std::mutex> lk(mu);
     for (auto& e : memo)
-        if (e.first.first == device && e.first.second == smem) return e.second;
-    const int nc = pair_clusters_kind3(smem, grid);
-    memo.push_back({{device, smem}, nc});
+        if (e.first.first == device && e.first.second == key) return e.second;
+    const int nc = pair_clusters_kind3(smem, grid, cluster);
+    memo.push_back({{device, key}, nc});
     return nc;
 }
 
@@ -662,6 +666,17 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
             grid = pair ? 2 * units : units;
         }
     }
+    // Quad mode: every unit one half of one large token tile in pair mode --
+    // the two pairs of a tile form one 4-CTA cluster and the contributor's
+    // partial moves to the finisher through DSMEM (when all those clusters
+    // are co-resident).
+    uint32_t cluster = pair ? 2u : 1u;
+    p.quad = 0;
+    if (pair && units == 2 * tiles && BN / 16 > kSentinelMaxChunks && G.KB % 2 == 0 && !K.no_quad &&
+        pair_clusters(w->device, smem, 2 * units, 4) >= int(tiles)) {
+        p.quad = 1;
+        cluster = 4;
+    }
     // Hybrid schedule: whole-tile rounds first, stream-K over the last G..2G
     // tiles (all tiles when there are fewer than G), tiles rasterized in groups
     // of GM token tiles sized so that the activation and weight slices of one
@@ -687,6 +702,7 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
     ks.pair = pair;
     ks.fan = n_fan > 0;
     ks.pdl = !K.no_pdl;
+    ks.cluster = cluster;
     ks.grid = grid;
     ks.smem = smem;
     ks.stream = stream;

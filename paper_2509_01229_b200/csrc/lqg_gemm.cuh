@@ -134,13 +134,15 @@ struct GemmParams {
     uint32_t tiles;            // weight-tile x token-tile pairs (summed over groups)
     uint32_t sk_q, sk_r;       // stream-K iterations (tiles after the DP rounds x KB) = sk_q * units + sk_r
     uint32_t acc_stages;       // at most this many accumulator stages in TMEM (1 or 2; see tmem_plan)
+    uint32_t quad;             // 1: clusters of 4 = the two CTA pairs of one split tile (units = 2 x tiles,
+                               //    pair mode): the partial moves through DSMEM, not L2 (see the epilogue)
 };
 
 // Shared memory after the rings and barriers: TMEM address holder, then the
 // token scales of the current tile (double).
 constexpr uint32_t kMiscTsOff = 128;
 constexpr uint32_t kMiscBytes = kMiscTsOff + kMaxBN * 8;
-constexpr uint32_t kNumBarriers = 4 * kMaxStages + 3 * kMaxASlots + 8;
+constexpr uint32_t kNumBarriers = 4 * kMaxStages + 3 * kMaxASlots + 9;
 
 // Grouped launch (MoE experts of one layer: same n, k, group size): the
 // tiles of every group form one linear space, tile-major within a group.
@@ -304,7 +306,7 @@ __device__ __forceinline__ TileRef tile_ref(uint32_t t, const GemmParams& p, con
     TileRef r;
     r.wimg = e.wimg;
     r.cs = e.cs;
-    r.nt = p.pair ? 2 * nt + ptx::cluster_ctarank() : nt;
+    r.nt = p.pair ? 2 * nt + (ptx::cluster_ctarank() & 1u) : nt;
     r.row0 = e.row0 + mt * p.BN;
     r.mlim = e.row0 + e.M;
     return r;
@@ -528,7 +530,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // gather reuses the rings; the order also runs through the MMA, this
     // makes it explicit)
     const uint32_t dq_done = bar_base + 8 * (kB + 3 * kMaxASlots + 7);
-    uint8_t* misc = smem + ((ring_bytes + 7) & ~7u) + 8 * (kB + 3 * kMaxASlots + 8);
+    // quad mode: the finisher's ring is free and its fin_bar armed (remote arrive)
+    const uint32_t qready = bar_base + 8 * (kB + 3 * kMaxASlots + 8);
+    uint8_t* misc = smem + ((ring_bytes + 7) & ~7u) + 8 * (kB + 3 * kMaxASlots + 9);
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(misc);
     double* ts_s = reinterpret_cast<double*>(misc + kMiscTsOff);  // kMaxBN token scales, as double
     uint32_t* team_info = reinterpret_cast<uint32_t*>(misc + 64);  // team finish: tile, acc column, nb
@@ -538,9 +542,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t KB = p.KB;
     constexpr uint32_t kTmemCols = 512;
     const TmemPlan tp = tmem_plan(p.BN, p.acc_stages);
-    const uint32_t rank = kPair ? ptx::cluster_ctarank() : 0u;  // 0 = pair leader
+    // cluster = one CTA pair, or (p.quad) the two pairs of one split tile
+    const uint32_t crank = kPair ? ptx::cluster_ctarank() : 0u;
+    const uint32_t rank = crank & 1u;   // 0 = pair leader
+    const uint32_t lead = crank & ~1u;  // the pair leader's cluster rank
     // barriers the pair leader waits on, as seen from this CTA
-    auto leader = [&](uint32_t bar) { return kPair ? ptx::mapa(bar, 0) : bar; };
+    auto leader = [&](uint32_t bar) { return kPair ? ptx::mapa(bar, lead) : bar; };
 
     if (threadIdx.x == 0) LQG_T(0);
     if (warp == 0) {
@@ -567,6 +574,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_init(team_ready, 1);         // the epilogue's leading thread
             ptx::mbar_init(team_done, kDQWarps);   // one arrive per dequant warp
             ptx::mbar_init(dq_done, kDQWarps);
+            ptx::mbar_init(qready, 1);
         }
         ptx::fence_mbar_init();
     }
@@ -653,7 +661,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     // both halves count on the leader's barrier; the leader expects the whole tile
                     if (rank == 0) ptx::mbar_arrive_expect_tx(xfull_bar(x.s), 2 * p.x_slot_bytes);
                     const int32_t m0 = int32_t(xrow0 + rank * (p.BN / 2));
-                    const uint32_t fb = ptx::mapa(xfull_bar(x.s), 0);
+                    const uint32_t fb = ptx::mapa(xfull_bar(x.s), lead);
                     ptx::tma_2d_g2s_pair(slot, &tmap_x, k0, m0, fb, pol_x);
                     ptx::tma_2d_g2s_pair(slot + atom_bytes, &tmap_x, k0 + int32_t(kXAtom), m0, fb, pol_x);
                 } else {
@@ -711,7 +719,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         auto commit = [&](uint32_t bar) {
             if (kPair)
-                ptx::mma_commit_pair(bar);
+                ptx::mma_commit_pair(bar, uint16_t(3u << lead));
             else
                 ptx::mma_commit(bar);
         };
@@ -1025,6 +1033,39 @@ __global__ void __launch_bounds__(kThreads, 1)
                     LQG_SEG(eidx, 9, c_st);
                 }
 #endif
+            } else if (kb0 > 0 && kPair && p.quad) {
+                // Quad mode: this pair holds the second half of the tile's
+                // k-range and the finisher pair is in the same cluster (ranks
+                // crank - 2). This is the CTA's only segment, so its rings are
+                // idle: stage the INT32 partial in shared memory ([chunk][quad]
+                // [row] int4 cells, the finisher's layout) and move it with one
+                // DSMEM bulk copy once the finisher's ring is free -- no L2
+                // round trip, no fence, no flag.
+                const uint32_t part_bytes = p.BN * kTileN * 4;
+                if (et == 0) ptx::mbar_wait(dq_done, 0);  // the W ring's last reads are done
+                epi_bar();
+                int4* sm4w = reinterpret_cast<int4*>(smem);
+                for (uint32_t ch = 0; ch < nchunks; ++ch) {
+                    uint32_t v[16];
+                    ptx::tmem_ld_x16(acc_taddr + ch * 16, v);
+                    ptx::tmem_ld_wait();
+                    if (ch + 1 == nchunks) release_acc(cur_as);
+#pragma unroll
+                    for (uint32_t q = 0; q < 4; ++q)
+                        sm4w[ch * 4 * kTileN + q * kTileN + row] =
+                            make_int4(int32_t(v[4 * q]), int32_t(v[4 * q + 1]), int32_t(v[4 * q + 2]),
+                                      int32_t(v[4 * q + 3]));
+                }
+                ptx::fence_proxy_async();  // the staged cells, for the bulk copy (async proxy)
+                epi_bar();
+                if (et == 0) {
+                    ptx::mbar_wait(qready, 0);  // the finisher's ring is free, its fin_bar armed
+                    ptx::bulk_s2s_cluster(ptx::mapa(smem_base, crank - 2), smem_base, part_bytes,
+                                          ptx::mapa(fin_bar, crank - 2));
+                    LQG_T(7);
+                }
+                // (the source cells stay valid until the copy completes: the
+                // finisher reaches the closing cluster barrier only after it)
             } else if (kb0 > 0) {
                 // Contributor piece of a split tile (always this CTA's first
                 // segment): publish the INT32 partial into this CTA's cells.
@@ -1135,7 +1176,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (uint32_t c0 = c_first;; c0 += nb_max) {
                         const uint32_t nb = min(nb_max, c_end - c0);
                         const bool last_batch = c0 + nb >= c_end;
-                        if (et == 0 && nb) {
+                        if (kPair && p.quad && et == 0 && nb) {
+                            // quad mode: the other half's pair (ranks crank + 2)
+                            // copies its partial into this ring (DSMEM)
+                            ptx::mbar_wait(dq_done, 0);  // the W ring's last reads are done
+                            ptx::mbar_arrive_expect_tx(fin_bar, part_bytes);
+                            ptx::fence_proxy_async();  // prior generic ring reads vs the async-proxy writes
+                            ptx::mbar_arrive_cluster(ptx::mapa(qready, crank + 2));
+                        } else if (et == 0 && nb) {
                             ptx::mbar_wait(dq_done, 0);  // the W ring's last reads are done
                             // The thread that issues the copies acquires every
                             // contributor's flag itself (then one proxy fence

@@ -31,7 +31,7 @@ cudaError_t launch(const KernelSpec& k, const GT& gt) {
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = k.pdl ? 1 : 0;
     attr[1].id = cudaLaunchAttributeClusterDimension;
-    attr[1].val.clusterDim.x = kPair ? 2 : 1;
+    attr[1].val.clusterDim.x = kPair ? k.cluster : 1;
     attr[1].val.clusterDim.y = 1;
     attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
@@ -51,7 +51,7 @@ cudaError_t LQG_CAT(launch_gemm_kind, LQG_KIND)(const KernelSpec& k) {
     return launch<1, false, false>(k, g1);
 }
 
-int LQG_CAT(pair_clusters_kind, LQG_KIND)(size_t smem, uint32_t grid) {
+int LQG_CAT(pair_clusters_kind, LQG_KIND)(size_t smem, uint32_t grid, uint32_t cluster) {
     if (smem_attr<1, false, true>() != cudaSuccess) return 0;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
@@ -59,7 +59,7 @@ int LQG_CAT(pair_clusters_kind, LQG_KIND)(size_t smem, uint32_t grid) {
     cfg.dynamicSmemBytes = smem;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.x = cluster;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;

@@ -19,6 +19,7 @@ struct KernelSpec {
     const GroupTable<kMaxGroups>* gt;  // the groups (ng > 1: grouped kernel)
     uint32_t ng;
     bool pair, fan, pdl;
+    uint32_t cluster;  // pair kernels: CTAs per cluster (2, or 4 in quad mode)
     uint32_t grid;
     size_t smem;
     cudaStream_t stream;
@@ -30,7 +31,7 @@ using PairClustersFn = int (*)(size_t smem, uint32_t grid);
 
 #define LQG_DECLARE_KIND(K)                               \
     cudaError_t launch_gemm_kind##K(const KernelSpec& k); \
-    int pair_clusters_kind##K(size_t smem, uint32_t grid); \
+    int pair_clusters_kind##K(size_t smem, uint32_t grid, uint32_t cluster); \
     int debug_trace_kind##K(unsigned long long* out);
 LQG_DECLARE_KIND(0)
 LQG_DECLARE_KIND(1)

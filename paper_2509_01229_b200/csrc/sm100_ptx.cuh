@@ -155,6 +155,14 @@ __device__ __forceinline__ void tma_2d_g2s(uint32_t dst, const CUtensorMap* map,
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async;" ::: "memory");
 }
+// Bulk copy from this CTA's shared memory into another CTA's of the cluster
+// (dst and bar: shared::cluster addresses from mapa), completing on that
+// CTA's mbarrier.
+__device__ __forceinline__ void bulk_s2s_cluster(uint32_t dst, uint32_t src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "r"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
 // Bulk prefetch of global memory into L2 (no shared-memory destination).
 __device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
@@ -302,11 +310,12 @@ __device__ __forceinline__ void mma_i8_ts_pair(uint32_t d_tmem, uint32_t a_tmem,
 }
 // Arrive on the mbarrier at this offset in both CTAs of the pair once the
 // issued tcgen05 ops complete.
-__device__ __forceinline__ void mma_commit_pair(uint32_t bar) {
+// `mask`: the pair's two cluster ranks (0b11 << leader rank).
+__device__ __forceinline__ void mma_commit_pair(uint32_t bar, uint16_t mask) {
     asm volatile(
         "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
             bar),
-        "h"(uint16_t(3))
+        "h"(mask)
         : "memory");
 }
 

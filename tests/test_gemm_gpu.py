@@ -696,6 +696,27 @@ def test_split_k_sequence_stress(torch_cuda, lqg):
                 assert torch.equal(acc, ref)
 
 
+@pytest.mark.parametrize("m,n,k", [(128, 8192, 2048), (64, 8192, 4096), (128, 4096, 28672), (100, 2048, 2048)])
+def test_quad_cluster_split_k_exact(torch_cuda, lqg, m, n, k):
+    """Quad mode (tiles split into two halves whose CTA pairs form one 4-CTA
+    cluster; the contributor's INT32 partial reaches the finisher through a
+    DSMEM bulk copy): exact accumulators against a float64 product of the
+    dequantized weights, F32 / BF16 outputs identical to the L2-exchange
+    path (no_quad), over repeated back-to-back launches."""
+    torch = torch_cuda
+    g = torch.Generator(device="cuda").manual_seed(m * 7 + n + k)
+    dw = lqg.DeviceWeights.quantize(torch.randn(n, k, generator=g, device="cuda") * 0.02, 128)
+    q, ts = lqg.quantize_activations(torch.randn(m, k, generator=g, device="cuda"))
+    ref = (q.to(torch.float64) @ dw.dequant().to(torch.float64).T).to(torch.int32)
+    with lqg.tune(no_quad=1):
+        y32 = dw.gemm(q, ts, out_dtype=torch.float32).clone()
+        ybf = dw.gemm(q, ts).clone()
+    for _ in range(8):
+        assert torch.equal(dw.gemm_accum(q), ref)
+        assert torch.equal(dw.gemm(q, ts, out_dtype=torch.float32), y32)
+        assert torch.equal(dw.gemm(q, ts), ybf)
+
+
 def test_tune_rejects_unknown_and_out_of_range(lqg):
     with pytest.raises(lqg.ValidationError):
         lqg.tune_set("no_such_knob", 1)

@@ -6,8 +6,9 @@ the CPU oracle so a sanitizer-perturbed schedule is also a correctness run:
 
 Cases: decode (1 token tile, sentinel split-K), mid-M one-CTA kernel with the
 flag + TMA-gather split-K, the CTA-pair kernel (cta_group::2, remote
-mbarrier arrivals), a grouped (MoE) launch with an empty expert, the
-fan-out epilogue into two destinations, and the GPU quantizers.
+mbarrier arrivals), the quad mode (4-CTA clusters, DSMEM split-K exchange),
+a grouped (MoE) launch with an empty expert, the fan-out epilogue into two
+destinations, and the GPU quantizers.
 """
 import os
 import sys
@@ -51,6 +52,8 @@ case(1024, 4096, 16)
 case(1024, 4096, 48, tune=dict(pair=0))
 # CTA pairs, two token tiles, ragged m
 dw, xq, tsd, y_ref = case(1024, 2048, 200, tune=dict(pair=1, max_bn=128))
+# quad mode: two CTA pairs per split tile in one 4-CTA cluster, DSMEM exchange
+case(2048, 2048, 128, tune=dict(pair=1))
 # fan-out epilogue: the same tile into two destinations
 outs = [torch.empty(200, 1024, dtype=torch.float32, device="cuda") for _ in range(2)]
 dw2, xq2, tsd2, y_ref2 = case(1024, 2048, 24)
