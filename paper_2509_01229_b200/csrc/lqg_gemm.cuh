@@ -46,9 +46,15 @@
 //
 // Work split: whole-tile rounds, then stream-K over the remaining tiles'
 // (tile, k-block) space. A tile whose k-range spans several CTAs is reduced
-// exactly in INT32 through a workspace (see the epilogue); integer addition
-// is associative, so results are bit-identical to the reference's fixed-order
-// sum in any arrival order.
+// exactly in INT32 through a workspace (see the epilogue) -- or, in quad mode
+// (two CTA pairs per tile in one 4-CTA cluster), by one DSMEM bulk copy from
+// the contributor pair's shared memory into the finisher pair's; integer
+// addition is associative, so results are bit-identical to the reference's
+// fixed-order sum in any arrival order.
+//
+// CTA pairs (kPair): cluster rank bit 0 is the position in the pair (0 =
+// leader, which issues the cta_group::2 MMAs), bit 1 (quad mode) the half of
+// the tile's k-range.
 #pragma once
 #include <cstdint>
 #include <cuda.h>
