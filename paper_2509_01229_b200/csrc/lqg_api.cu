@@ -361,7 +361,7 @@ constexpr uint32_t kSmemMisc = (1024 + 8 * kNumBarriers + 8 + kMiscBytes + 1023)
 // tests change them through lqg_tune_set (process-wide, no environment reads).
 enum TuneId : int {
     kTuneMaxBN, kTunePairMinM, kTunePair, kTunePairSingleTile, kTuneXRingBytes, kTuneMaxXStages,
-    kTuneMaxWStages, kTuneGrid, kTuneRasterGM, kTuneNoDP, kTuneNoPDL, kTuneAccStages, kTuneHostChunkM, kTuneHostChunks, kTuneNoQuad, kTuneCount
+    kTuneMaxWStages, kTuneGrid, kTuneRasterGM, kTuneNoDP, kTuneNoPDL, kTuneAccStages, kTuneHostChunkM, kTuneHostChunks, kTuneNoQuad, kTuneAutoTile, kTuneCount
 };
 struct TuneDef {
     const char* name;
@@ -383,18 +383,19 @@ constexpr TuneDef kTuneDefs[kTuneCount] = {
     {"host_chunk_m", 384, 1, 1 << 30},             // host-buffer calls of >= this many rows are pipelined
     {"host_chunks", 6, 1, 8},                      // ... in this many row chunks
     {"no_quad", 0, 0, 1},                          // 1: split tiles exchange through L2 even where a 4-CTA cluster fits
+    {"auto_tile", 1, 0, 1},                        // token-tile / pair rules for few or short-K tiles (see pick_tiles)
 };
 std::atomic<int64_t> g_tune[kTuneCount] = {
     {kTuneDefs[0].dflt}, {kTuneDefs[1].dflt}, {kTuneDefs[2].dflt}, {kTuneDefs[3].dflt},
     {kTuneDefs[4].dflt}, {kTuneDefs[5].dflt}, {kTuneDefs[6].dflt}, {kTuneDefs[7].dflt},
     {kTuneDefs[8].dflt}, {kTuneDefs[9].dflt}, {kTuneDefs[10].dflt}, {kTuneDefs[11].dflt},
-    {kTuneDefs[12].dflt}, {kTuneDefs[13].dflt}, {kTuneDefs[14].dflt}};
+    {kTuneDefs[12].dflt}, {kTuneDefs[13].dflt}, {kTuneDefs[14].dflt}, {kTuneDefs[15].dflt}};
 
 struct Knobs {
     uint32_t max_bn, pair_min_m;
     int pair;
     uint32_t pair_single_tile, x_ring_bytes, max_x_stages, max_w_stages, grid, raster_gm, no_dp, no_pdl, acc_stages, host_chunk_m,
-        host_chunks, no_quad;
+        host_chunks, no_quad, auto_tile;
 };
 Knobs knobs() {
     auto g = [](TuneId i) { return g_tune[i].load(std::memory_order_relaxed); };
@@ -414,6 +415,7 @@ Knobs knobs() {
     k.host_chunk_m = uint32_t(g(kTuneHostChunkM));
     k.host_chunks = uint32_t(g(kTuneHostChunks));
     k.no_quad = uint32_t(g(kTuneNoQuad));
+    k.auto_tile = uint32_t(g(kTuneAutoTile));
     return k;
 }
 
@@ -422,6 +424,62 @@ uint32_t choose_bn(uint32_t m, uint32_t cap, uint32_t* mt) {
     const uint32_t per = (m + MT - 1) / MT;
     *mt = MT;
     return std::max(16u, (per + 15) / 16 * 16);
+}
+
+// Token-tile cap and CTA-pair policy for a single GEMM under the default
+// knobs (auto_tile). The base rule (fewest token tiles of <= 192 tokens,
+// pairs from pair_min_m tokens) is tuned on the LLaMA-2-70B shapes; three
+// measured corrections for GEMMs with few weight tiles or a short k
+// (tools/sched_sweep.py on B200, every variant bit-identical):
+//  A  k < 32 k-blocks and >= 2 rounds of pair tiles: no pairs. With 16
+//     k-blocks per tile the pair kernel's per-tile cost shows (LLaMA-2-7B
+//     gate_up M = 256 / 512 / 1024: 32.4 -> 30.6, 53.3 -> 48.5,
+//     91.4 -> 85.8 us; qkv M = 1024 56.3 -> 51.5 us).
+//  B  one round of whole pair tiles that leaves units idle (T <= U < 2T,
+//     no split): more, smaller token tiles while they still fit in one round
+//     and stay >= 128 tokens (7B o M = 512 15.1 -> 13.4 us, down M = 512
+//     27.3 -> 23.5 us).
+//  C  split tiles (2T <= U: halves or equal pieces): halve the token tile
+//     instead, if each CTA's weight stream of the 2T smaller tiles stays
+//     within the equal-piece bound -- short k streams its whole tile faster
+//     than a split reduces (7B o M = 256 13.4 -> 11.5 us, down M = 128
+//     17.9 -> 17.1 us; not for down at M = 256, whose 43 k-blocks per tile
+//     stream 731 KB per CTA: 19.5 -> 24.7 us measured).
+// Returns the token-tile cap and sets *pair_pol (-1 auto, 0 never).
+uint32_t pick_tiles(const ImageGeom& G, uint32_t m, uint32_t num_sms, uint32_t pair_min_m, int* pair_pol) {
+    constexpr uint64_t kPieceBytes = 400u * 1024u;  // the equal-piece bound of launch_core
+    uint32_t mt;
+    const uint32_t bn = choose_bn(m, kMaxTileM, &mt);
+    const uint32_t units_np = std::min<uint32_t>(num_sms, kMaxSlots), units_p = units_np / 2;
+    if (m < pair_min_m || G.NT % 2 != 0 || units_p < 1) return kMaxTileM;
+    const uint32_t ntp = G.NT / 2;
+    auto pair_bn = [&](uint32_t t) {
+        uint32_t x;
+        const uint32_t b = choose_bn((m + t - 1) / t, kMaxTileM, &x);
+        return std::min(kMaxTileM, (b + 31) / 32 * 32);
+    };
+    const uint64_t T = uint64_t(ntp) * mt;
+    if (G.KB < 32 && T >= 2ull * units_p) {  // A
+        *pair_pol = 0;
+        return kMaxTileM;
+    }
+    const uint32_t bnp = std::min(kMaxTileM, (bn + 31) / 32 * 32);
+    if (bnp < 128) return kMaxTileM;
+    if (T <= units_p && 2 * T > units_p) {  // B
+        uint32_t best = 0;
+        for (uint32_t t = mt + 1; t <= 4 * mt; ++t) {
+            if (pair_bn(t) < 128 || uint64_t(ntp) * t > units_p) break;
+            best = t;
+        }
+        return best ? pair_bn(best) : kMaxTileM;
+    }
+    if (2 * T <= units_p) {  // C
+        const uint32_t t = 2 * mt, b = pair_bn(t);
+        const uint64_t T2 = uint64_t(ntp) * t;
+        const uint64_t pp = T2 ? units_p / T2 : 0;
+        if (pp >= 1 && uint64_t(G.KB) * G.chunk_bytes / pp <= kPieceBytes) return b;
+    }
+    return kMaxTileM;
 }
 
 // Activation tensor maps, cached per thread: encoding one costs ~1 us of host
@@ -495,7 +553,7 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
                 const int8_t* d_x, int64_t ldx, const float* d_ts, void* d_out, int64_t ldo,
                 uint32_t out_kind, lqg_workspace* ws, cudaStream_t stream,
                 void* const* fan = nullptr, uint32_t n_fan = 0) {
-    const Knobs K = knobs();
+    Knobs K = knobs();
     const lqg_weights* w = ws_list[0];
     const ImageGeom& G = w->geom;
     uint64_t rows = 0;
@@ -532,6 +590,8 @@ int launch_core(const lqg_weights* const* ws_list, uint32_t ng, const uint32_t* 
 
     // Token tile from the largest group; every group gets ceil(m_e / BN) tiles.
     uint32_t MT;
+    if (K.auto_tile && ng == 1 && n_fan == 0 && K.max_bn == kMaxTileM && K.pair == -1)
+        K.max_bn = pick_tiles(G, max_m, w->num_sms, K.pair_min_m, &K.pair);
     uint32_t BN = choose_bn(max_m, K.max_bn, &MT);
     // CTA pairs (tcgen05 cta_group::2) for multi-token-tile GEMMs: the two
     // CTAs of a cluster own adjacent weight tiles and each loads half of the

@@ -257,8 +257,8 @@ LLAMA70B = [("qkv", 10240, 8192), ("o", 8192, 8192), ("gate_up", 28672, 8192), (
 
 @pytest.mark.parametrize("shape", [s[0] for s in LLAMA7B])
 def test_llama7b_shapes_bf16_and_acc(torch_cuda, lqg, port, shape):
-    """BASELINE configs[1]: every LLaMA-2-7B layer GEMM at M = 1, 16, 256 and
-    1024 (the bench's sweep points) -- INT32 accumulators bit-exact, the F32
+    """BASELINE configs[1]: every LLaMA-2-7B layer GEMM at M = 1, 16, 128, 256,
+    512 and 1024 (bench sweep points; 128-1024 run the auto_tile schedules) -- INT32 accumulators bit-exact, the F32
     output bit-identical and the BF16 output (what the bench times) exactly the
     RNE of the reference F32 on a seeded subset of rows and columns."""
     torch = torch_cuda
@@ -270,7 +270,7 @@ def test_llama7b_shapes_bf16_and_acc(torch_cuda, lqg, port, shape):
     cols = np.sort(rng.choice(n, size=192, replace=False))
     w8 = port.reconstruct_int8(len(cols), k, 128, port.logical_codes(n, k, 0, e.packed_weights)[cols],
                                e.group_scales.reshape(n, -1)[cols], e.group_offsets.reshape(n, -1)[cols])
-    for m in (1, 16, 256, 1024):
+    for m in (1, 16, 128, 256, 512, 1024):
         q, ts = lqg.quantize_activations(torch.randn(m, k, generator=g, device="cuda"))
         acc = dw.gemm_accum(q).cpu().numpy()
         y32 = dw.gemm(q, ts, out_dtype=torch.float32).cpu().numpy()
@@ -281,6 +281,24 @@ def test_llama7b_shapes_bf16_and_acc(torch_cuda, lqg, port, shape):
         np.testing.assert_array_equal(y32[np.ix_(rows, cols)].view(np.uint32), y_ref.view(np.uint32))
         assert torch.equal(y16.cpu()[torch.from_numpy(rows)][:, torch.from_numpy(cols)],
                            torch.from_numpy(y_ref).to(torch.bfloat16))
+
+
+@pytest.mark.parametrize("shape", [s[0] for s in LLAMA7B])
+def test_auto_tile_schedules_match_base_rule(torch_cuda, lqg, shape):
+    """The auto_tile corrections (pick_tiles: no pairs for short k, smaller
+    token tiles to fill the units, whole tiles instead of split halves) only
+    move the schedule: full INT32 and BF16 outputs equal the base rule's
+    (auto_tile=0) at every M where they change it."""
+    torch = torch_cuda
+    _, n, k = next(s for s in LLAMA7B if s[0] == shape)
+    g = torch.Generator(device="cuda").manual_seed(n + k)
+    dw = lqg.DeviceWeights.quantize(torch.randn(n, k, generator=g, device="cuda") * 0.02, 128)
+    for m in (128, 256, 384, 512, 768, 1024):
+        q, ts = lqg.quantize_activations(torch.randn(m, k, generator=g, device="cuda"))
+        acc1, y1 = dw.gemm_accum(q), dw.gemm(q, ts)
+        with lqg.lq.tune(auto_tile=0):
+            acc0, y0 = dw.gemm_accum(q), dw.gemm(q, ts)
+        assert torch.equal(acc0, acc1) and torch.equal(y0, y1), m
 
 
 @pytest.mark.parametrize("m", [16, 4096])
