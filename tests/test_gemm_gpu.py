@@ -741,3 +741,45 @@ def test_tune_rejects_unknown_and_out_of_range(lqg):
     with pytest.raises(lqg.ValidationError):
         lqg.tune_set("max_w_stages", 1)
     assert lqg.tune_get("pair") == -1
+
+
+@pytest.mark.parametrize("m,n,k", [(4096, 8192, 8192), (1000, 4096, 4096), (300, 2048, 1024)])
+def test_bf16_equals_rne_of_f32_full_output(torch_cuda, lqg, m, n, k):
+    """Every BF16 output equals RNE of the F32 output (itself bit-identical to
+    the reference epilogue, quant.cpp:125-127) over the full matrix -- at
+    4096 x 8192 that includes ~10^4 values within a few float ulps of a BF16
+    rounding midpoint, where a single-rounding FP32 shortcut would differ."""
+    torch = torch_cuda
+    g = torch.Generator(device="cuda").manual_seed(m + n + k)
+    dw = lqg.DeviceWeights.quantize(torch.randn(n, k, generator=g, device="cuda") * 0.02, 128)
+    q, ts = lqg.quantize_activations(torch.randn(m, k, generator=g, device="cuda"))
+    y32 = dw.gemm(q, ts, out_dtype=torch.float32)
+    y16 = dw.gemm(q, ts, out_dtype=torch.bfloat16)
+    assert torch.equal(y16, y32.to(torch.bfloat16))
+
+
+def test_extreme_scales_bit_exact(torch_cuda, lqg, port):
+    """Channel and token scales far from the usual range (tiny, huge, zero
+    token scales): F32 bit-identical to the reference epilogue, F16/BF16 its
+    RNE (F16 overflows to inf exactly where the reference F32 does)."""
+    torch = torch_cuda
+    rng = np.random.default_rng(77)
+    m, n, k, g = 200, 256, 512, 128
+    b = port.build_bundle_plain(make_weights(rng, n, k), g)
+    cs = b["channel_scales"].copy()
+    cs[:6] = [1e-30, 3e-19, 1e20, 2.5e25, 7e-18, 1e18]
+    b["channel_scales"] = cs.astype(np.float32)
+    q, ts = port.quantize_activations(make_acts(rng, m, k))
+    ts = ts.copy()
+    ts[[0, 17, 33, 150]] = [0.0, 1e-25, 1e12, 5e9]
+    ts = ts.astype(np.float32)
+    acc_ref, y_ref = port.gemm_oracle(q, ts, port.bundle_int8(b), b["channel_scales"])
+    assert np.isinf(y_ref).any() and (y_ref == 0).any()
+    dw = lqg.DeviceWeights.from_bundle(to_bundle(lqg, b), 0)
+    xq = torch.from_numpy(np.ascontiguousarray(q)).cuda()
+    tsd = torch.from_numpy(np.ascontiguousarray(ts)).cuda()
+    np.testing.assert_array_equal(dw.gemm_accum(xq).cpu().numpy().astype(np.int64), acc_ref.astype(np.int64))
+    y = dw.gemm(xq, tsd, out_dtype=torch.float32).cpu().numpy()
+    np.testing.assert_array_equal(y.view(np.uint32), y_ref.view(np.uint32))
+    for dt in (torch.float16, torch.bfloat16):
+        assert torch.equal(dw.gemm(xq, tsd, out_dtype=dt).cpu(), torch.from_numpy(y_ref).to(dt))
