@@ -348,7 +348,11 @@ constexpr uint32_t kMaxTileM = 192;
 // tile: one M = 256 MMA per k-block serves two SMs, which halves the MMA
 // warp's per-k-block overhead per SM (LLaMA-2-70B 4-GEMM step on B200:
 // M = 128 117 -> 110 us, M = 256 176 -> 159 us; M = 16 unchanged either way).
-constexpr uint32_t kPairMinM = 48;
+// Below 80 tokens one-CTA tiles are faster (tools/sched_sweep.py, 4-GEMM
+// steps: 70B at M = 48 89.1 -> 84.3 us, M = 64 89.7 -> 88.6; 7B at M = 48
+// 53.2 -> 47.1 and M = 64 53.2 -> 49.3 with pick_tiles' rule D), from 96
+// tokens pairs win (70B M = 96 94.8 vs 97.8 us without).
+constexpr uint32_t kPairMinM = 80;
 constexpr uint32_t kDecodeWStages = 6;  // W ring depth for token tiles <= 32
 // Dynamic shared memory: the two rings, then barriers / schedule / token scales.
 
@@ -448,6 +452,15 @@ uint32_t choose_bn(uint32_t m, uint32_t cap, uint32_t* mt) {
 // Returns the token-tile cap and sets *pair_pol (-1 auto, 0 never).
 uint32_t pick_tiles(const ImageGeom& G, uint32_t m, uint32_t num_sms, uint32_t pair_min_m, int* pair_pol) {
     constexpr uint64_t kPieceBytes = 400u * 1024u;  // the equal-piece bound of launch_core
+    // D  small weights (<= 12 MB, e.g. 7B o 4096 x 4096) at 33-128 tokens:
+    //    32-token one-CTA tiles -- the cheap sentinel split-K and MT passes
+    //    over L2-resident weights beat a few large split tiles (7B o M = 64 /
+    //    96 / 128: 11.3 -> 8.4, 12.4 -> 9.1, 11.2 -> 9.4 us; 7B down, 23 MB,
+    //    measured slower at M >= 96, so the bound).
+    if (m > 32 && m <= 128 && uint64_t(G.NT) * G.KB * G.chunk_bytes <= (12ull << 20)) {
+        *pair_pol = 0;
+        return 32;
+    }
     uint32_t mt;
     const uint32_t bn = choose_bn(m, kMaxTileM, &mt);
     const uint32_t units_np = std::min<uint32_t>(num_sms, kMaxSlots), units_p = units_np / 2;
