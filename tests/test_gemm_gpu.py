@@ -286,14 +286,15 @@ def test_llama7b_shapes_bf16_and_acc(torch_cuda, lqg, port, shape):
 @pytest.mark.parametrize("shape", [s[0] for s in LLAMA7B])
 def test_auto_tile_schedules_match_base_rule(torch_cuda, lqg, shape):
     """The auto_tile corrections (pick_tiles: no pairs for short k, smaller
-    token tiles to fill the units, whole tiles instead of split halves) only
+    token tiles to fill the units, whole tiles instead of split halves,
+    32-token tiles for small weights) only
     move the schedule: full INT32 and BF16 outputs equal the base rule's
     (auto_tile=0) at every M where they change it."""
     torch = torch_cuda
     _, n, k = next(s for s in LLAMA7B if s[0] == shape)
     g = torch.Generator(device="cuda").manual_seed(n + k)
     dw = lqg.DeviceWeights.quantize(torch.randn(n, k, generator=g, device="cuda") * 0.02, 128)
-    for m in (128, 256, 384, 512, 768, 1024):
+    for m in (48, 64, 96, 128, 256, 384, 512, 768, 1024):
         q, ts = lqg.quantize_activations(torch.randn(m, k, generator=g, device="cuda"))
         acc1, y1 = dw.gemm_accum(q), dw.gemm(q, ts)
         with lqg.lq.tune(auto_tile=0):
