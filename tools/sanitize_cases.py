@@ -50,6 +50,9 @@ def case(n, k, m, tune=None):
 case(1024, 4096, 16)
 # mid-M, one-CTA kernel, 3 token chunks -> flag + TMA-gather split-K
 case(1024, 4096, 48, tune=dict(pair=0))
+# small weights at 96 tokens (auto_tile rule D): three 32-token tiles on the
+# one-CTA kernel, sentinel split-K per tile
+case(1024, 4096, 96)
 # CTA pairs, two token tiles, ragged m
 dw, xq, tsd, y_ref = case(1024, 2048, 200, tune=dict(pair=1, max_bn=128))
 # quad mode: two CTA pairs per split tile in one 4-CTA cluster, DSMEM exchange
