@@ -242,7 +242,9 @@ uint64_t lqg_kernel_launch_count(void);
  * "max_x_stages", "max_w_stages" (ring depths are rounded down to even),
  * "grid", "raster_gm", "no_dp", "no_pdl", "acc_stages" (1: one accumulator
  * stage and a deeper TMEM A ring), "no_quad" (1: split tiles exchange
- * partials through L2 even where 4-CTA clusters fit), and for the host-buffer
+ * partials through L2 even where 4-CTA clusters fit), "auto_tile" (0: skip
+ * the short-k / few-tile / small-weight token-tile and pair corrections;
+ * they apply only while "max_bn" and "pair" keep their defaults), and for the host-buffer
  * calls "host_chunk_m", "host_chunks" (row-chunk pipelining).
  * Results are bit-identical under every setting; only the schedule changes.
  * Unknown names and out-of-range values -> LQG_EVALIDATION. */
